@@ -1,0 +1,721 @@
+/*
+ * oracle.c — CPU ORACLE. TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * leg may load or call this library.  The product path (paper_0709_1272_b200/) never
+ * links, imports or executes anything under oracle/, and this file shares no code,
+ * header, table or helper with the CUDA path.
+ *
+ * What it is: a plain, slow, obviously-correct FP64 implementation of the three tiled
+ * factorizations of the paper (arXiv 0709.1272, PAPER.md = /root/reference/PAPER.md):
+ *   - Tiled Cholesky  — Algorithm 1 (alg:blkchol), kernels DPOTF2 /
+ *     DTRSM / DGSMM.
+ *   - Tiled QR        — Algorithm 2 (alg:blkqr), kernels DGEQRT /
+ *     DLARFB / DTSQRT / DSSRFB with inner blocking s = ib
+ *     (§3.2.3).
+ *   - Tiled LU with incremental (tiled pairwise) pivoting — Algorithm 3 (alg:blklu,
+ *     PAPER.md:560-576), kernels DGETRF / DGESSM / DTSTRF / DSSSSM,
+ *     L-strip storage per the footnote at PAPER.md:542-544.
+ * Every kernel is written in the order and notation of SURVEY.md §8(c) C1-C3 (the
+ * readings of the paper this build adopts, listed in DESIGN.md §3).  Drivers run the
+ * algorithms in program order; there is no blocking, fusion or reordering beyond what
+ * the algorithm states.  Plain loops, no BLAS; compile with -O2 -ffp-contract=off so
+ * that no FMA contraction changes the rounding of the written formulas.
+ *
+ * Also: brute-force references (unblocked Cholesky, unblocked Householder QR, GEPP,
+ * GEWP) and the C4 checks (residuals, implicit application of Q and of N).
+ *
+ * Layout ("Block Data Layout"): p = n/b tiles per
+ * side; tile (i,j) (0-based) starts at element (i + j*p)*b*b and is column-major
+ * inside.  T strips (QR) and L strips (LU): strip (i,k) at (i + k*p)*ib*b, an
+ * ib x b column-major block; inner block s occupies strip columns [s*ib, (s+1)*ib).
+ * Pivots: int32, vector (i,k) at (i + k*p)*b, 1-based; GETRF in [1,b], TSTRF in
+ * [1,2b] with bottom row r encoded as b+r+1.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OT(A, p, b, i, j) ((A) + ((size_t)(i) + (size_t)(j) * (size_t)(p)) * (size_t)(b) * (size_t)(b))
+#define OE(X, ld, r, c) ((X)[(size_t)(r) + (size_t)(c) * (size_t)(ld)])
+#define OSTRIP(S, p, b, ib, i, k) ((S) + ((size_t)(i) + (size_t)(k) * (size_t)(p)) * (size_t)(ib) * (size_t)(b))
+#define OPIV(P, p, b, i, k) ((P) + ((size_t)(i) + (size_t)(k) * (size_t)(p)) * (size_t)(b))
+
+/* ------------------------------------------------------------------------------------
+ * Layout conversion (SPEC.md:41-56 from_dense / to_dense).  Dense is column-major m x n.
+ * ---------------------------------------------------------------------------------- */
+void o_pack(int64_t m, int64_t n, int64_t b, const double* dense, double* tiles) {
+  int64_t p = m / b;
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t r = 0; r < m; ++r) {
+      int64_t i = r / b, j = c / b;
+      OE(OT(tiles, p, b, i, j), b, r % b, c % b) = OE(dense, m, r, c);
+    }
+}
+
+void o_unpack(int64_t m, int64_t n, int64_t b, const double* tiles, double* dense) {
+  int64_t p = m / b;
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t r = 0; r < m; ++r) {
+      int64_t i = r / b, j = c / b;
+      OE(dense, m, r, c) = OE(OT(tiles, p, b, i, j), b, r % b, c % b);
+    }
+}
+
+/* ====================================================================================
+ * C1 — Cholesky kernels
+ * ================================================================================== */
+
+/* DPOTF2: A_kk -> L_kk = chol(A_kk), lower, positive diagonal
+ * ("unit" at PAPER.md:262 read as an erratum).  Reads/writes the lower
+ * triangle only; the strict upper triangle is never touched (Z2).
+ * Returns 0, or the 1-based local column whose pivot d is not > 0 (LAPACK info, Z3). */
+int o_potrf(int64_t b, double* A) {
+  for (int64_t j = 0; j < b; ++j) {
+    double d = OE(A, b, j, j);
+    for (int64_t m = 0; m < j; ++m) d -= OE(A, b, j, m) * OE(A, b, j, m);
+    if (!(d > 0.0)) return (int)(j + 1);
+    double ljj = sqrt(d);
+    OE(A, b, j, j) = ljj;
+    for (int64_t r = j + 1; r < b; ++r) {
+      double s = OE(A, b, r, j);
+      for (int64_t m = 0; m < j; ++m) s -= OE(A, b, r, m) * OE(A, b, j, m);
+      OE(A, b, r, j) = s / ljj;
+    }
+  }
+  return 0;
+}
+
+/* DTRSM: L_ik = A_ik L_kk^{-T}; row by row,
+ * X[r,c] = (A[r,c] - sum_{m<c} X[r,m] L[c,m]) / L[c,c]. */
+void o_trsm(int64_t b, const double* L, double* A) {
+  for (int64_t r = 0; r < b; ++r)
+    for (int64_t c = 0; c < b; ++c) {
+      double s = OE(A, b, r, c);
+      for (int64_t m = 0; m < c; ++m) s -= OE(A, b, r, m) * OE(L, b, c, m);
+      OE(A, b, r, c) = s / OE(L, b, c, c);
+    }
+}
+
+/* DGSMM, diagonal case ("take advantage of their triangular
+ * structure"): C -= A A^T on the lower triangle only (SYRK; Z2). */
+void o_syrk(int64_t b, const double* A, double* C) {
+  for (int64_t c = 0; c < b; ++c)
+    for (int64_t r = c; r < b; ++r) {
+      double s = OE(C, b, r, c);
+      for (int64_t m = 0; m < b; ++m) s -= OE(A, b, r, m) * OE(A, b, c, m);
+      OE(C, b, r, c) = s;
+    }
+}
+
+/* DGSMM, off-diagonal case: C -= A B^T. */
+void o_gemm_nt(int64_t b, const double* A, const double* B, double* C) {
+  for (int64_t c = 0; c < b; ++c)
+    for (int64_t r = 0; r < b; ++r) {
+      double s = OE(C, b, r, c);
+      for (int64_t m = 0; m < b; ++m) s -= OE(A, b, r, m) * OE(B, b, c, m);
+      OE(C, b, r, c) = s;
+    }
+}
+
+/* Algorithm 1 in program order.  Returns 0 or the first failing
+ * global column (1-based); on failure stops writing (Z3). */
+int o_chol(int64_t n, int64_t b, double* A) {
+  int64_t p = n / b;
+  for (int64_t k = 0; k < p; ++k) {
+    int info = o_potrf(b, OT(A, p, b, k, k));
+    if (info) return (int)(k * b + info);
+    for (int64_t i = k + 1; i < p; ++i) o_trsm(b, OT(A, p, b, k, k), OT(A, p, b, i, k));
+    for (int64_t i = k + 1; i < p; ++i)
+      for (int64_t j = k + 1; j <= i; ++j) {
+        if (i == j) o_syrk(b, OT(A, p, b, i, k), OT(A, p, b, i, i));
+        else o_gemm_nt(b, OT(A, p, b, i, k), OT(A, p, b, j, k), OT(A, p, b, i, j));
+      }
+  }
+  return 0;
+}
+
+/* ====================================================================================
+ * C2 — QR kernels (inner blocking §3.2.3)
+ * ================================================================================== */
+
+/* House(alpha, x): LAPACK dlarfg semantics without the safmin rescaling loop (Z6).
+ * On return x holds v, *alpha holds beta; returns tau. */
+static double o_house(double* alpha, double* x, int64_t len, int64_t stride) {
+  double ss = 0.0;
+  for (int64_t r = 0; r < len; ++r) ss += x[r * stride] * x[r * stride];
+  double xn = sqrt(ss);
+  if (xn == 0.0) {
+    return 0.0; /* tau = 0, beta = alpha, v = x = 0 */
+  }
+  double a = *alpha;
+  double nrm = sqrt(a * a + xn * xn);
+  double beta = (a >= 0.0) ? -nrm : nrm;
+  double tau = (beta - a) / beta;
+  double den = a - beta;
+  for (int64_t r = 0; r < len; ++r) x[r * stride] = x[r * stride] / den;
+  *alpha = beta;
+  return tau;
+}
+
+/* T_s column jj of the forward columnwise compact-WY factor (dlarft):
+ * T[jj,jj] = tau_j, T[0:jj,jj] = T[0:jj,0:jj] * w with w = -tau_j * (V[:,c0:j]^T v_j).
+ * `w` is passed in (already holding V^T v_j); Ts is ib x ib, column-major ld ib. */
+static void o_tcol(double* Ts, int64_t ib, int64_t jj, double tau, double* w) {
+  for (int64_t m = 0; m < jj; ++m) w[m] = -tau * w[m];
+  for (int64_t r = 0; r < jj; ++r) {
+    double s = 0.0;
+    for (int64_t m = r; m < jj; ++m) s += OE(Ts, ib, r, m) * w[m];
+    OE(Ts, ib, r, jj) = s;
+  }
+  OE(Ts, ib, jj, jj) = tau;
+  for (int64_t r = jj + 1; r < ib; ++r) OE(Ts, ib, r, jj) = 0.0;
+}
+
+/* Element (r, m) of the unit-lower reflector block V_s of a GEQRT'ed tile, rows
+ * counted in the tile: 1 on the diagonal (r == c0+m), the stored v below, 0 above. */
+static double o_vgeq(const double* A, int64_t b, int64_t c0, int64_t r, int64_t m) {
+  int64_t c = c0 + m;
+  if (r < c) return 0.0;
+  if (r == c) return 1.0;
+  return OE(A, b, r, c);
+}
+
+/* Apply the block reflector of inner block s of GEQRT'ed tile V (T strip Tst) to
+ * rows c0..b-1 of C (b x ncol, ld ldc): C <- (I - V_s op(T_s) V_s^T) C with
+ * op = T^T when trans != 0 (the factorization, Q^T), op = T when trans == 0 (Q). */
+static void o_apply_geq_block(int64_t b, int64_t ib, int64_t s, const double* V, const double* Tst,
+                              double* C, int64_t ldc, int64_t ncol, int trans) {
+  int64_t c0 = s * ib;
+  const double* Ts = Tst + (size_t)c0 * ib;
+  double* W = (double*)malloc(sizeof(double) * ib * (ncol > 0 ? ncol : 1));
+  double* W2 = (double*)malloc(sizeof(double) * ib * (ncol > 0 ? ncol : 1));
+  for (int64_t c = 0; c < ncol; ++c)
+    for (int64_t m = 0; m < ib; ++m) {
+      double acc = 0.0;
+      for (int64_t r = c0; r < b; ++r) acc += o_vgeq(V, b, c0, r, m) * OE(C, ldc, r, c);
+      OE(W, ib, m, c) = acc;
+    }
+  for (int64_t c = 0; c < ncol; ++c)
+    for (int64_t m = 0; m < ib; ++m) {
+      double acc = 0.0;
+      for (int64_t q = 0; q < ib; ++q)
+        acc += (trans ? OE(Ts, ib, q, m) : OE(Ts, ib, m, q)) * OE(W, ib, q, c);
+      OE(W2, ib, m, c) = acc;
+    }
+  for (int64_t c = 0; c < ncol; ++c)
+    for (int64_t r = c0; r < b; ++r) {
+      double acc = 0.0;
+      for (int64_t m = 0; m < ib; ++m) acc += o_vgeq(V, b, c0, r, m) * OE(W2, ib, m, c);
+      OE(C, ldc, r, c) -= acc;
+    }
+  free(W);
+  free(W2);
+}
+
+/* DGEQRT with inner block ib: A -> (V strict lower, R upper,
+ * T strip).  C2: per inner block, panel Householder, T_s (dlarft), trailing update. */
+void o_geqrt(int64_t b, int64_t ib, double* A, double* Tst) {
+  double* w = (double*)malloc(sizeof(double) * ib);
+  for (int64_t s = 0; s * ib < b; ++s) {
+    int64_t c0 = s * ib, c1 = c0 + ib;
+    double* Ts = Tst + (size_t)c0 * ib;
+    for (int64_t j = c0; j < c1; ++j) {
+      double tau = o_house(&OE(A, b, j, j), &OE(A, b, j + 1, j), b - j - 1, 1);
+      /* apply H_j = I - tau [1;v][1;v]^T to A[j:b, j+1:c1] */
+      for (int64_t c = j + 1; c < c1; ++c) {
+        double wc = OE(A, b, j, c);
+        for (int64_t r = j + 1; r < b; ++r) wc += OE(A, b, r, j) * OE(A, b, r, c);
+        OE(A, b, j, c) -= tau * wc;
+        for (int64_t r = j + 1; r < b; ++r) OE(A, b, r, c) -= tau * wc * OE(A, b, r, j);
+      }
+      /* T_s column: w[m] = V[:, c0+m]^T v_j over rows >= j */
+      int64_t jj = j - c0;
+      for (int64_t m = 0; m < jj; ++m) {
+        double acc = OE(A, b, j, c0 + m); /* v_j has 1 at row j */
+        for (int64_t r = j + 1; r < b; ++r) acc += OE(A, b, r, c0 + m) * OE(A, b, r, j);
+        w[m] = acc;
+      }
+      o_tcol(Ts, ib, jj, tau, w);
+    }
+    if (c1 < b) o_apply_geq_block(b, ib, s, A, Tst, &OE(A, b, 0, c1), b, b - c1, 1);
+  }
+  free(w);
+}
+
+/* DLARFB: A_kj <- Q_kk^T A_kj, i.e. (I - V_s T_s^T V_s^T) for
+ * s = 0..t-1 in order (reading Z5). */
+void o_larfb(int64_t b, int64_t ib, const double* V, const double* Tst, double* C) {
+  for (int64_t s = 0; s * ib < b; ++s) o_apply_geq_block(b, ib, s, V, Tst, C, b, b, 1);
+}
+
+/* Block reflector of a TSQRT'ed pair: top rows c0..c1-1 of X1 (identity part of V),
+ * bottom all b rows of X2 (dense V_s = Vb[:, c0:c1]).
+ * trans != 0: X <- (I - V T^T V^T) X, else (I - V T V^T) X. */
+static void o_apply_ts_block(int64_t b, int64_t ib, int64_t s, const double* Vb, const double* Tst,
+                             double* X1, int64_t ld1, double* X2, int64_t ld2, int64_t ncol,
+                             int trans) {
+  int64_t c0 = s * ib;
+  const double* Ts = Tst + (size_t)c0 * ib;
+  double* W = (double*)malloc(sizeof(double) * ib * (ncol > 0 ? ncol : 1));
+  double* W2 = (double*)malloc(sizeof(double) * ib * (ncol > 0 ? ncol : 1));
+  for (int64_t c = 0; c < ncol; ++c)
+    for (int64_t m = 0; m < ib; ++m) {
+      double acc = OE(X1, ld1, c0 + m, c);
+      for (int64_t r = 0; r < b; ++r) acc += OE(Vb, b, r, c0 + m) * OE(X2, ld2, r, c);
+      OE(W, ib, m, c) = acc;
+    }
+  for (int64_t c = 0; c < ncol; ++c)
+    for (int64_t m = 0; m < ib; ++m) {
+      double acc = 0.0;
+      for (int64_t q = 0; q < ib; ++q)
+        acc += (trans ? OE(Ts, ib, q, m) : OE(Ts, ib, m, q)) * OE(W, ib, q, c);
+      OE(W2, ib, m, c) = acc;
+    }
+  for (int64_t c = 0; c < ncol; ++c) {
+    for (int64_t m = 0; m < ib; ++m) OE(X1, ld1, c0 + m, c) -= OE(W2, ib, m, c);
+    for (int64_t r = 0; r < b; ++r) {
+      double acc = 0.0;
+      for (int64_t m = 0; m < ib; ++m) acc += OE(Vb, b, r, c0 + m) * OE(W2, ib, m, c);
+      OE(X2, ld2, r, c) -= acc;
+    }
+  }
+  free(W);
+  free(W2);
+}
+
+/* DTSQRT (inner blocking PAPER.md:637-647): QR of [R; A] with R the
+ * upper triangle of the diagonal tile (only its upper region is read or written) and
+ * A a full tile; A <- V_ik (top part implicitly identity), T strip written. */
+void o_tsqrt(int64_t b, int64_t ib, double* R, double* A, double* Tst) {
+  double* w = (double*)malloc(sizeof(double) * ib);
+  for (int64_t s = 0; s * ib < b; ++s) {
+    int64_t c0 = s * ib, c1 = c0 + ib;
+    double* Ts = Tst + (size_t)c0 * ib;
+    for (int64_t j = c0; j < c1; ++j) {
+      double tau = o_house(&OE(R, b, j, j), &OE(A, b, 0, j), b, 1);
+      for (int64_t c = j + 1; c < c1; ++c) {
+        double wc = OE(R, b, j, c);
+        for (int64_t r = 0; r < b; ++r) wc += OE(A, b, r, j) * OE(A, b, r, c);
+        OE(R, b, j, c) -= tau * wc;
+        for (int64_t r = 0; r < b; ++r) OE(A, b, r, c) -= tau * wc * OE(A, b, r, j);
+      }
+      int64_t jj = j - c0;
+      for (int64_t m = 0; m < jj; ++m) {
+        double acc = 0.0; /* top parts e_{c0+m}, e_j are orthogonal */
+        for (int64_t r = 0; r < b; ++r) acc += OE(A, b, r, c0 + m) * OE(A, b, r, j);
+        w[m] = acc;
+      }
+      o_tcol(Ts, ib, jj, tau, w);
+    }
+    if (c1 < b) o_apply_ts_block(b, ib, s, A, Tst, &OE(R, b, 0, c1), b, &OE(A, b, 0, c1), b, b - c1, 1);
+  }
+  free(w);
+}
+
+/* DSSRFB: [R_kj; A_ij] <- Q_ik^T [R_kj; A_ij],
+ * inner blocks s = 0..t-1 in order. */
+void o_ssrfb(int64_t b, int64_t ib, const double* V, const double* Tst, double* R, double* A) {
+  for (int64_t s = 0; s * ib < b; ++s) o_apply_ts_block(b, ib, s, V, Tst, R, b, A, b, b, 1);
+}
+
+/* Algorithm 2, square p x p tiles, in program order. */
+void o_qr(int64_t n, int64_t b, int64_t ib, double* A, double* T) {
+  int64_t p = n / b;
+  for (int64_t k = 0; k < p; ++k) {
+    o_geqrt(b, ib, OT(A, p, b, k, k), OSTRIP(T, p, b, ib, k, k));
+    for (int64_t j = k + 1; j < p; ++j)
+      o_larfb(b, ib, OT(A, p, b, k, k), OSTRIP(T, p, b, ib, k, k), OT(A, p, b, k, j));
+    for (int64_t i = k + 1; i < p; ++i) {
+      o_tsqrt(b, ib, OT(A, p, b, k, k), OT(A, p, b, i, k), OSTRIP(T, p, b, ib, i, k));
+      for (int64_t j = k + 1; j < p; ++j)
+        o_ssrfb(b, ib, OT(A, p, b, i, k), OSTRIP(T, p, b, ib, i, k), OT(A, p, b, k, j), OT(A, p, b, i, j));
+    }
+  }
+}
+
+/* C4: X (n x ncol, column-major, ld n) <- Q X (trans == 0) or Q^T X (trans != 0),
+ * Q the orthogonal factor held implicitly by the factored tiles and T strips.
+ * Q X applies the inverses of the factorization's block reflectors in reverse task
+ * order and reverse inner-block order, with T untransposed. */
+void o_qr_apply(int64_t n, int64_t b, int64_t ib, const double* F, const double* T, double* X,
+                int64_t ncol, int trans) {
+  int64_t p = n / b, t = b / ib;
+  if (trans) {
+    for (int64_t k = 0; k < p; ++k) {
+      for (int64_t s = 0; s < t; ++s)
+        o_apply_geq_block(b, ib, s, OT(F, p, b, k, k), OSTRIP(T, p, b, ib, k, k), X + k * b, n, ncol, 1);
+      for (int64_t i = k + 1; i < p; ++i)
+        for (int64_t s = 0; s < t; ++s)
+          o_apply_ts_block(b, ib, s, OT(F, p, b, i, k), OSTRIP(T, p, b, ib, i, k), X + k * b, n,
+                           X + i * b, n, ncol, 1);
+    }
+  } else {
+    for (int64_t k = p - 1; k >= 0; --k) {
+      for (int64_t i = p - 1; i > k; --i)
+        for (int64_t s = t - 1; s >= 0; --s)
+          o_apply_ts_block(b, ib, s, OT(F, p, b, i, k), OSTRIP(T, p, b, ib, i, k), X + k * b, n,
+                           X + i * b, n, ncol, 0);
+      for (int64_t s = t - 1; s >= 0; --s)
+        o_apply_geq_block(b, ib, s, OT(F, p, b, k, k), OSTRIP(T, p, b, ib, k, k), X + k * b, n, ncol, 0);
+    }
+  }
+}
+
+/* ====================================================================================
+ * C3 — LU kernels (storage PAPER.md:536-546 and footnote)
+ * ================================================================================== */
+
+static void o_swap_rows(double* X, int64_t ld, int64_t r1, int64_t r2, int64_t c0, int64_t c1) {
+  if (r1 == r2) return;
+  for (int64_t c = c0; c < c1; ++c) {
+    double tmp = OE(X, ld, r1, c);
+    OE(X, ld, r1, c) = OE(X, ld, r2, c);
+    OE(X, ld, r2, c) = tmp;
+  }
+}
+
+/* DGETRF: P A = L U with partial pivoting inside the tile, LAPACK
+ * dgetrf semantics with block ib (Z12: whole-tile-row swaps).  First argmax of fabs
+ * over rows j..b-1 (idamax rule, Z11).  *info gets the first zero-pivot local column
+ * (1-based) if none recorded yet. */
+void o_getrf(int64_t b, int64_t ib, double* A, int32_t* ipiv, int* info) {
+  for (int64_t s = 0; s * ib < b; ++s) {
+    int64_t c0 = s * ib, c1 = c0 + ib;
+    for (int64_t j = c0; j < c1; ++j) {
+      int64_t r = j;
+      double best = fabs(OE(A, b, j, j));
+      for (int64_t rr = j + 1; rr < b; ++rr)
+        if (fabs(OE(A, b, rr, j)) > best) { best = fabs(OE(A, b, rr, j)); r = rr; }
+      ipiv[j] = (int32_t)(r + 1);
+      if (OE(A, b, r, j) != 0.0) {
+        o_swap_rows(A, b, j, r, 0, b);
+        for (int64_t rr = j + 1; rr < b; ++rr) OE(A, b, rr, j) /= OE(A, b, j, j);
+      } else if (*info == 0) {
+        *info = (int)(j + 1);
+      }
+      for (int64_t c = j + 1; c < c1; ++c)
+        for (int64_t rr = j + 1; rr < b; ++rr) OE(A, b, rr, c) -= OE(A, b, rr, j) * OE(A, b, j, c);
+    }
+    if (c1 < b) {
+      /* A[c0:c1, c1:b] <- L_ss^{-1} A[c0:c1, c1:b] (unit lower) */
+      for (int64_t c = c1; c < b; ++c)
+        for (int64_t r = c0; r < c1; ++r) {
+          double acc = OE(A, b, r, c);
+          for (int64_t m = c0; m < r; ++m) acc -= OE(A, b, r, m) * OE(A, b, m, c);
+          OE(A, b, r, c) = acc;
+        }
+      /* A[c1:b, c1:b] -= A[c1:b, c0:c1] A[c0:c1, c1:b] */
+      for (int64_t c = c1; c < b; ++c)
+        for (int64_t r = c1; r < b; ++r) {
+          double acc = OE(A, b, r, c);
+          for (int64_t m = c0; m < c1; ++m) acc -= OE(A, b, r, m) * OE(A, b, m, c);
+          OE(A, b, r, c) = acc;
+        }
+    }
+  }
+}
+
+/* DGESSM: A_kj <- L_kk^{-1} P_kk A_kj — all swaps, then the blocked
+ * unit-lower forward solve. */
+void o_gessm(int64_t b, int64_t ib, const double* L, const int32_t* ipiv, double* A) {
+  for (int64_t j = 0; j < b; ++j) o_swap_rows(A, b, j, ipiv[j] - 1, 0, b);
+  for (int64_t s = 0; s * ib < b; ++s) {
+    int64_t c0 = s * ib, c1 = c0 + ib;
+    for (int64_t c = 0; c < b; ++c)
+      for (int64_t r = c0; r < c1; ++r) {
+        double acc = OE(A, b, r, c);
+        for (int64_t m = c0; m < r; ++m) acc -= OE(L, b, r, m) * OE(A, b, m, c);
+        OE(A, b, r, c) = acc;
+      }
+    for (int64_t c = 0; c < b; ++c)
+      for (int64_t r = c1; r < b; ++r) {
+        double acc = OE(A, b, r, c);
+        for (int64_t m = c0; m < c1; ++m) acc -= OE(L, b, r, m) * OE(A, b, m, c);
+        OE(A, b, r, c) = acc;
+      }
+  }
+}
+
+/* DTSTRF (footnote PAPER.md:542-544): pairwise-pivoted LU of [U; A]
+ * with U the upper triangle of the diagonal tile (only its upper region is touched),
+ * A a full tile.  A <- bottom multipliers, Ls strip <- the t unit-lower ib x ib blocks
+ * (strictly lower part stored), ipiv in [1,2b].  Reading C3 / Z10 / Z11 / Z13. */
+void o_tstrf(int64_t b, int64_t ib, double* U, double* A, double* Ls, int32_t* ipiv, int* info) {
+  for (int64_t s = 0; s * ib < b; ++s) {
+    int64_t c0 = s * ib, c1 = c0 + ib;
+    for (int64_t c = c0; c < c1; ++c)
+      for (int64_t r = 0; r < ib; ++r) OE(Ls, ib, r, c) = 0.0;
+    for (int64_t j = c0; j < c1; ++j) {
+      int64_t r = -1;
+      double best = fabs(OE(U, b, j, j));
+      for (int64_t rr = 0; rr < b; ++rr)
+        if (fabs(OE(A, b, rr, j)) > best) { best = fabs(OE(A, b, rr, j)); r = rr; }
+      if (r >= 0) {
+        ipiv[j] = (int32_t)(b + r + 1);
+        for (int64_t c = j; c < c1; ++c) {
+          double tmp = OE(U, b, j, c); OE(U, b, j, c) = OE(A, b, r, c); OE(A, b, r, c) = tmp;
+        }
+        for (int64_t c = c0; c < j; ++c) {
+          double tmp = OE(Ls, ib, j - c0, c); OE(Ls, ib, j - c0, c) = OE(A, b, r, c); OE(A, b, r, c) = tmp;
+        }
+      } else {
+        ipiv[j] = (int32_t)(j + 1);
+      }
+      if (OE(U, b, j, j) != 0.0) {
+        for (int64_t rr = 0; rr < b; ++rr) OE(A, b, rr, j) /= OE(U, b, j, j);
+        for (int64_t c = j + 1; c < c1; ++c)
+          for (int64_t rr = 0; rr < b; ++rr) OE(A, b, rr, c) -= OE(A, b, rr, j) * OE(U, b, j, c);
+      } else if (*info == 0) {
+        *info = (int)(j + 1);
+      }
+    }
+    if (c1 < b) {
+      for (int64_t j = c0; j < c1; ++j)
+        if (ipiv[j] > b) {
+          int64_t r = ipiv[j] - b - 1;
+          for (int64_t c = c1; c < b; ++c) {
+            double tmp = OE(U, b, j, c); OE(U, b, j, c) = OE(A, b, r, c); OE(A, b, r, c) = tmp;
+          }
+        }
+      for (int64_t c = c1; c < b; ++c)
+        for (int64_t r = c0; r < c1; ++r) {
+          double acc = OE(U, b, r, c);
+          for (int64_t m = c0; m < r; ++m) acc -= OE(Ls, ib, r - c0, m) * OE(U, b, m, c);
+          OE(U, b, r, c) = acc;
+        }
+      for (int64_t c = c1; c < b; ++c)
+        for (int64_t r = 0; r < b; ++r) {
+          double acc = OE(A, b, r, c);
+          for (int64_t m = c0; m < c1; ++m) acc -= OE(A, b, r, m) * OE(U, b, m, c);
+          OE(A, b, r, c) = acc;
+        }
+    }
+  }
+}
+
+/* DSSSSM: [U_kj; A_ij] <- L_ik^{-1} P_ik [U_kj; A_ij] per inner block:
+ * swaps of whole rows, (I+Ls_s)^{-1} on the top rows, then A_ij -= L_ik[:,s] U_kj[s,:]. */
+void o_ssssm(int64_t b, int64_t ib, const double* L, const double* Ls, const int32_t* ipiv,
+             double* U, double* A) {
+  for (int64_t s = 0; s * ib < b; ++s) {
+    int64_t c0 = s * ib, c1 = c0 + ib;
+    for (int64_t j = c0; j < c1; ++j)
+      if (ipiv[j] > b) {
+        int64_t r = ipiv[j] - b - 1;
+        for (int64_t c = 0; c < b; ++c) {
+          double tmp = OE(U, b, j, c); OE(U, b, j, c) = OE(A, b, r, c); OE(A, b, r, c) = tmp;
+        }
+      }
+    for (int64_t c = 0; c < b; ++c)
+      for (int64_t r = c0; r < c1; ++r) {
+        double acc = OE(U, b, r, c);
+        for (int64_t m = c0; m < r; ++m) acc -= OE(Ls, ib, r - c0, m) * OE(U, b, m, c);
+        OE(U, b, r, c) = acc;
+      }
+    for (int64_t c = 0; c < b; ++c)
+      for (int64_t r = 0; r < b; ++r) {
+        double acc = OE(A, b, r, c);
+        for (int64_t m = c0; m < c1; ++m) acc -= OE(L, b, r, m) * OE(U, b, m, c);
+        OE(A, b, r, c) = acc;
+      }
+  }
+}
+
+/* Algorithm 3, square p x p tiles, program order.  Returns 0 or the
+ * smallest global column (1-based) whose pivot was exactly zero. */
+int o_lu(int64_t n, int64_t b, int64_t ib, double* A, double* Ls, int32_t* ipiv) {
+  int64_t p = n / b;
+  int64_t best = 0;
+  for (int64_t k = 0; k < p; ++k) {
+    int info = 0;
+    o_getrf(b, ib, OT(A, p, b, k, k), OPIV(ipiv, p, b, k, k), &info);
+    if (info && (best == 0 || k * b + info < best)) best = k * b + info;
+    for (int64_t j = k + 1; j < p; ++j)
+      o_gessm(b, ib, OT(A, p, b, k, k), OPIV(ipiv, p, b, k, k), OT(A, p, b, k, j));
+    for (int64_t i = k + 1; i < p; ++i) {
+      info = 0;
+      o_tstrf(b, ib, OT(A, p, b, k, k), OT(A, p, b, i, k), OSTRIP(Ls, p, b, ib, i, k),
+              OPIV(ipiv, p, b, i, k), &info);
+      if (info && (best == 0 || k * b + info < best)) best = k * b + info;
+      for (int64_t j = k + 1; j < p; ++j)
+        o_ssssm(b, ib, OT(A, p, b, i, k), OSTRIP(Ls, p, b, ib, i, k), OPIV(ipiv, p, b, i, k),
+                OT(A, p, b, k, j), OT(A, p, b, i, j));
+    }
+  }
+  return (int)best;
+}
+
+/* C4 / Eq. (eq:formula N), (eq:GETWPcompact):
+ * X (n x ncol, ld n) <- N X, N = (prod of the elementary L and P of GETWP)^{-1},
+ * applied implicitly by undoing every elimination step in reverse program order. */
+void o_lu_apply_N(int64_t n, int64_t b, int64_t ib, const double* F, const double* Ls,
+                  const int32_t* ipiv, double* X, int64_t ncol) {
+  int64_t p = n / b, t = b / ib;
+  for (int64_t k = p - 1; k >= 0; --k) {
+    double* x1 = X + k * b;
+    for (int64_t i = p - 1; i > k; --i) {
+      const double* L = OT(F, p, b, i, k);
+      const double* Lst = OSTRIP(Ls, p, b, ib, i, k);
+      const int32_t* pv = OPIV(ipiv, p, b, i, k);
+      double* x2 = X + i * b;
+      for (int64_t s = t - 1; s >= 0; --s) {
+        int64_t c0 = s * ib, c1 = c0 + ib;
+        for (int64_t c = 0; c < ncol; ++c) {
+          /* x2 += L[:, c0:c1] x1[c0:c1] (uses x1 before its update) */
+          for (int64_t r = 0; r < b; ++r) {
+            double acc = 0.0;
+            for (int64_t m = c0; m < c1; ++m) acc += OE(L, b, r, m) * OE(x1, n, m, c);
+            OE(x2, n, r, c) += acc;
+          }
+          /* x1[c0:c1] <- (I + Ls_s) x1[c0:c1]; rows descending so inputs stay original */
+          for (int64_t r = c1 - 1; r >= c0; --r) {
+            double acc = 0.0;
+            for (int64_t m = c0; m < r; ++m) acc += OE(Lst, ib, r - c0, m) * OE(x1, n, m, c);
+            OE(x1, n, r, c) += acc;
+          }
+        }
+        for (int64_t j = c1 - 1; j >= c0; --j)
+          if (pv[j] > b) {
+            int64_t r = pv[j] - b - 1;
+            for (int64_t c = 0; c < ncol; ++c) {
+              double tmp = OE(x1, n, j, c); OE(x1, n, j, c) = OE(x2, n, r, c); OE(x2, n, r, c) = tmp;
+            }
+          }
+      }
+    }
+    /* undo GETRF(k): x <- L_kk x (unit lower, full tile), then undo swaps in reverse */
+    const double* Lkk = OT(F, p, b, k, k);
+    const int32_t* pv = OPIV(ipiv, p, b, k, k);
+    for (int64_t c = 0; c < ncol; ++c)
+      for (int64_t r = b - 1; r >= 0; --r) {
+        double acc = 0.0;
+        for (int64_t m = 0; m < r; ++m) acc += OE(Lkk, b, r, m) * OE(x1, n, m, c);
+        OE(x1, n, r, c) += acc;
+      }
+    for (int64_t j = b - 1; j >= 0; --j) {
+      int64_t r = pv[j] - 1;
+      if (r != j)
+        for (int64_t c = 0; c < ncol; ++c) {
+          double tmp = OE(x1, n, j, c); OE(x1, n, j, c) = OE(x1, n, r, c); OE(x1, n, r, c) = tmp;
+        }
+    }
+  }
+}
+
+/* ====================================================================================
+ * Brute-force references (SURVEY §8(c) C5 "Brute force for n <= 64", "Special cases")
+ * Dense column-major n x n.
+ * ================================================================================== */
+
+/* Unblocked right-looking scalar Cholesky (textbook).  Lower triangle. */
+int o_ref_chol(int64_t n, double* A) {
+  for (int64_t k = 0; k < n; ++k) {
+    double d = OE(A, n, k, k);
+    if (!(d > 0.0)) return (int)(k + 1);
+    OE(A, n, k, k) = sqrt(d);
+    for (int64_t i = k + 1; i < n; ++i) OE(A, n, i, k) /= OE(A, n, k, k);
+    for (int64_t j = k + 1; j < n; ++j)
+      for (int64_t i = j; i < n; ++i) OE(A, n, i, j) -= OE(A, n, i, k) * OE(A, n, j, k);
+  }
+  return 0;
+}
+
+/* Unblocked Householder QR (dgeqr2): R upper, v below the diagonal, tau[n]. */
+void o_ref_qr(int64_t n, double* A, double* tau) {
+  for (int64_t j = 0; j < n; ++j) {
+    tau[j] = o_house(&OE(A, n, j, j), &OE(A, n, j + 1, j), n - j - 1, 1);
+    for (int64_t c = j + 1; c < n; ++c) {
+      double wc = OE(A, n, j, c);
+      for (int64_t r = j + 1; r < n; ++r) wc += OE(A, n, r, j) * OE(A, n, r, c);
+      OE(A, n, j, c) -= tau[j] * wc;
+      for (int64_t r = j + 1; r < n; ++r) OE(A, n, r, c) -= tau[j] * wc * OE(A, n, r, j);
+    }
+  }
+}
+
+/* Unblocked GEPP (dgetf2): ipiv 1-based, L strictly lower, U upper.  Returns info. */
+int o_ref_gepp(int64_t n, double* A, int32_t* ipiv) {
+  int info = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    int64_t r = j;
+    double best = fabs(OE(A, n, j, j));
+    for (int64_t rr = j + 1; rr < n; ++rr)
+      if (fabs(OE(A, n, rr, j)) > best) { best = fabs(OE(A, n, rr, j)); r = rr; }
+    ipiv[j] = (int32_t)(r + 1);
+    if (OE(A, n, r, j) != 0.0) {
+      o_swap_rows(A, n, j, r, 0, n);
+      for (int64_t rr = j + 1; rr < n; ++rr) OE(A, n, rr, j) /= OE(A, n, j, j);
+    } else if (!info) {
+      info = (int)(j + 1);
+    }
+    for (int64_t c = j + 1; c < n; ++c)
+      for (int64_t rr = j + 1; rr < n; ++rr) OE(A, n, rr, c) -= OE(A, n, rr, j) * OE(A, n, j, c);
+  }
+  return info;
+}
+
+/* GEWP — Gaussian elimination with pairwise pivoting (Wilkinson):
+ * for each column k, rows i = k+1..n-1 in order: row k and row i compete, the larger
+ * |entry| becomes row k (strictly greater wins), then row i -= l * row k with
+ * l = A[i,k]/A[k,k] stored in A[i,k].  swapped[k + i*n] = 1 when rows were exchanged. */
+int o_ref_gewp(int64_t n, double* A, int32_t* swapped) {
+  int info = 0;
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t i = k + 1; i < n; ++i) {
+      swapped[k + i * n] = 0;
+      if (fabs(OE(A, n, i, k)) > fabs(OE(A, n, k, k))) {
+        o_swap_rows(A, n, k, i, k, n);
+        swapped[k + i * n] = 1;
+      }
+      if (OE(A, n, k, k) != 0.0) {
+        double l = OE(A, n, i, k) / OE(A, n, k, k);
+        OE(A, n, i, k) = l;
+        for (int64_t c = k + 1; c < n; ++c) OE(A, n, i, c) -= l * OE(A, n, k, c);
+      } else if (!info) {
+        info = (int)(k + 1);
+      }
+    }
+  return info;
+}
+
+/* ====================================================================================
+ * Checks (C4)
+ * ================================================================================== */
+
+/* ||A - L L^T||_F / ||A||_F over the full symmetric A, where A_lo holds the lower
+ * triangle of A and L the factor, both dense column-major n x n. */
+double o_chol_residual(int64_t n, const double* A_lo, const double* L) {
+  double num = 0.0, den = 0.0;
+  for (int64_t c = 0; c < n; ++c)
+    for (int64_t r = c; r < n; ++r) {
+      double acc = 0.0;
+      for (int64_t m = 0; m <= c; ++m) acc += OE(L, n, r, m) * OE(L, n, c, m);
+      double a = OE(A_lo, n, r, c);
+      double e = a - acc;
+      double wgt = (r == c) ? 1.0 : 2.0;
+      num += wgt * e * e;
+      den += wgt * a * a;
+    }
+  return sqrt(num) / sqrt(den);
+}
+
+/* Leading-order flop counts per task kind. */
+double o_kernel_flops(int kind, double b, double s) {
+  switch (kind) {
+    case 0: return b * b * b / 3.0;          /* POTRF */
+    case 1: return b * b * b;                /* TRSM */
+    case 2: return b * b * (b + 1.0);        /* SYRK */
+    case 3: return 2.0 * b * b * b;          /* GEMM */
+    case 4: return 4.0 * b * b * b / 3.0;    /* GEQRT */
+    case 5: return 2.0 * b * b * b + 3.0 * s * b * b;  /* LARFB (approx.) */
+    case 6: return 2.0 * b * b * b + s * b * b;        /* TSQRT */
+    case 7: return 4.0 * b * b * b + s * b * b;        /* SSRFB */
+    case 8: return 2.0 * b * b * b / 3.0;    /* GETRF */
+    case 9: return b * b * b;                /* GESSM */
+    case 10: return b * b * b + s * b * b / 2.0;       /* TSTRF */
+    case 11: return 2.0 * b * b * b + s * b * b;       /* SSSSM */
+    default: return 0.0;
+  }
+}

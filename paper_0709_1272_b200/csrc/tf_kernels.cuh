@@ -1,0 +1,818 @@
+// tf_kernels.cuh — the eleven tile kernels of Algorithms 1-3 as CTA-wide device
+// functions (256 threads, one work item each), called by the persistent scheduler
+// (tf_lib.cu) and by the per-kernel test launcher tk_run.
+//
+//   Cholesky:  POTRF, TRSM, SYRK (DGSMM i=j), GEMM (DGSMM i>j)
+//   QR:  GEQRT, LARFB, TSQRT, SSRFB   (inner block ib, §3.2.3)
+//   LU:  GETRF, GESSM, TSTRF, SSSSM   (L strips)
+//
+// Semantics follow SURVEY.md §8(c) C1-C3 (the readings adopted in DESIGN.md §3); the
+// arithmetic is blocked for the hardware (DMMA engine for every dense update, warp-level
+// panels), so results agree with the oracle to rounding, and bitwise on the exact pins.
+//
+// Work items: update tasks are split so several CTAs work on one task — TRSM by
+// 128-row blocks, SYRK/GEMM by 128x128 output sub-tiles, LARFB/SSRFB/GESSM/SSSSM by
+// column slabs of NS columns.  Panel tasks (POTRF/GEQRT/TSQRT/GETRF/TSTRF) are one item.
+//
+// Memory-model notes: tile data is read with L2-only loads (cp.async.cg / ld.global.cg)
+// or through shared memory; tasks that write only the R/U ("up") region of a diagonal
+// tile store element by element inside that region, never over V/L.
+#pragma once
+#include <climits>
+#include "tf_gemm.cuh"
+
+namespace tf {
+
+constexpr int SMEM_DOUBLES = 25600;  // 200 KB dynamic shared memory per CTA
+constexpr int RB = 128;              // TRSM row block / SYRK-GEMM sub-tile edge
+constexpr int NS = 64;               // column-slab width of LARFB/SSRFB/GESSM/SSSSM items
+constexpr int NB = 32;               // column block of the in-CTA POTRF / TRSM solves
+
+struct Ctx {
+  int b, ib;
+  double* scratch;  // this CTA's global scratch (>= 2*ib*b + 64 doubles)
+  int* info;        // INT_MAX = no failure; atomicMin of the 1-based global column
+  int* abort_flag;  // set on Cholesky failure: the scheduler stops handing out work
+};
+
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------------ item counts
+__host__ __device__ inline int items_of(int kind, int b) {
+  const int nr = ceil_div(b, RB);
+  switch (kind) {
+    case 1: return nr;                 // TRSM: row blocks
+    case 2: return nr * (nr + 1) / 2;  // SYRK: lower sub-tiles
+    case 3: return nr * nr;            // GEMM: sub-tiles
+    case 5: case 7: case 9: case 11: return ceil_div(b, NS);  // slabs
+    default: return 1;                 // panels
+  }
+}
+
+using GemmNT128 = Gemm<128, 128, 2, 4, false, false>;
+using GemmNT32 = Gemm<128, 32, 4, 2, false, false>;
+using GemmW64 = Gemm<64, 64, 2, 4, true, true>;
+using GemmW32 = Gemm<32, 128, 1, 8, true, true>;
+using GemmUpd = Gemm<128, 64, 4, 2, false, true>;
+
+// C(M x N, ldc) -= Aop * Bop over tiles of the update engine (A m-contig, B k-major).
+__device__ inline void update_mn(double* sm, double* C, int ldc, const double* A, int lda, const double* B,
+                                 int ldb, int M, int N, int K) {
+  for (int n0 = 0; n0 < N; n0 += 64)
+    for (int m0 = 0; m0 < M; m0 += 128) {
+      GemmUpd g;
+      g.zero();
+      const int mm = min(128, M - m0), nn = min(64, N - n0);
+      g.run(sm, A + m0, lda, B + (size_t)n0 * ldb, ldb, mm, nn, K);
+      sub_store(g, C + m0 + (size_t)n0 * ldc, ldc, mm, nn);
+    }
+}
+
+// W(M x N, ld ldw) = Aop^T-style product with both operands k-major (+ optional addend
+// R(M x N, ldr) read from global), written to W.  Used for W = V^T C (+ R).
+__device__ inline void w_product(double* sm, double* W, int ldw, const double* A, int lda, const double* B,
+                                 int ldb, int M, int N, int K, const double* R, int ldr) {
+  if (M <= 32) {
+    for (int n0 = 0; n0 < N; n0 += 128) {
+      GemmW32 g;
+      g.zero();
+      const int nn = min(128, N - n0);
+      g.run(sm, A, lda, B + (size_t)n0 * ldb, ldb, M, nn, K);
+      g.for_each(M, nn, [&](int r, int c, double v) {
+        const int cc = n0 + c;
+        W[r + (size_t)cc * ldw] = R ? v + ldg_cg(R + r + (size_t)cc * ldr) : v;
+      });
+    }
+  } else {
+    for (int m0 = 0; m0 < M; m0 += 64)
+      for (int n0 = 0; n0 < N; n0 += 64) {
+        GemmW64 g;
+        g.zero();
+        const int mm = min(64, M - m0), nn = min(64, N - n0);
+        g.run(sm, A + (size_t)m0 * lda, lda, B + (size_t)n0 * ldb, ldb, mm, nn, K);
+        g.for_each(mm, nn, [&](int r, int c, double v) {
+          const int rr = m0 + r, cc = n0 + c;
+          W[rr + (size_t)cc * ldw] = R ? v + ldg_cg(R + rr + (size_t)cc * ldr) : v;
+        });
+      }
+  }
+  __syncthreads();
+}
+
+// W2 = T^T W for an upper-triangular ib x ib T (smem, ld ldt): W2[m][n] = sum_{q<=m} T[q][m] W[q][n].
+__device__ inline void apply_tt(const double* sT, int ldt, const double* W, double* W2, int ib, int N) {
+  for (int e = threadIdx.x; e < ib * N; e += TF_THREADS) {
+    const int m = e % ib, n = e / ib;
+    double s = 0.0;
+    for (int q = 0; q <= m; ++q) s += sT[q + m * ldt] * W[q + (size_t)n * ib];
+    W2[m + (size_t)n * ib] = s;
+  }
+  __syncthreads();
+}
+
+// Load the T_s block (ib x ib) of strip Tst into shared memory (ld ib).
+__device__ inline void load_ts(double* sT, const double* Tst, int ib, int c0) {
+  for (int e = threadIdx.x; e < ib * ib; e += TF_THREADS) sT[e] = ldg_cg(Tst + (size_t)c0 * ib + e);
+  __syncthreads();
+}
+
+// ====================================================================================
+// Cholesky (C1)
+// ====================================================================================
+
+// In-place Cholesky of the nb x nb lower block D (smem, ld NB+1) by warp 0, left-looking
+// per column as in DPOTF2.  Returns -1 or the failing local column.
+__device__ inline int chol_diag_block(double* D, int nb, int* sflag) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int fail = -1;
+    for (int j = 0; j < nb; ++j) {
+      double s = 0.0;
+      if (lane >= j && lane < nb) {
+        s = D[lane + j * (NB + 1)];
+        for (int m = 0; m < j; ++m) s -= D[lane + m * (NB + 1)] * D[j + m * (NB + 1)];
+      }
+      const double d = __shfl_sync(0xffffffffu, s, j);
+      if (!(d > 0.0)) { fail = j; break; }
+      const double ljj = sqrt(d);
+      if (lane == j) D[j + j * (NB + 1)] = ljj;
+      else if (lane > j && lane < nb) D[lane + j * (NB + 1)] = s / ljj;
+      __syncwarp();
+    }
+    if (lane == 0) *sflag = fail;
+  }
+  __syncthreads();
+  return *sflag;
+}
+
+// X[r, 0:nb] <- X[r, 0:nb] * D^{-T} for rows r in [0, rows) (X global, ld ldx), D the
+// lower nb x nb block in smem (ld NB+1).  Row-parallel; right-looking inside a row:
+// X[r,c] = (A[r,c] - sum_{m<c} X[r,m] D[c,m]) / D[c,c] (DTRSM).
+__device__ inline void row_solve(double* X, int ldx, int rows, int nb, const double* D) {
+  for (int r = threadIdx.x; r < rows; r += TF_THREADS) {
+    double x[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) x[c] = (c < nb) ? ldg_cg(X + r + (size_t)c * ldx) : 0.0;
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      if (c < nb) {
+        x[c] = x[c] / D[c + c * (NB + 1)];
+#pragma unroll
+        for (int c2 = c + 1; c2 < NB; ++c2)
+          if (c2 < nb) x[c2] -= x[c] * D[c2 + c * (NB + 1)];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NB; ++c)
+      if (c < nb) X[r + (size_t)c * ldx] = x[c];
+  }
+}
+
+__device__ inline void load_lower_block(double* D, const double* A, int ld, int nb) {
+  for (int e = threadIdx.x; e < NB * NB; e += TF_THREADS) {
+    const int r = e % NB, c = e / NB;
+    D[r + c * (NB + 1)] = (r < nb && c < nb && r >= c) ? ldg_cg(A + r + (size_t)c * ld) : 0.0;
+  }
+  __syncthreads();
+}
+
+// POTRF (DPOTF2): blocked left-looking Cholesky of the b x b tile A.
+// Only the lower triangle is read or written (Z2).  Returns -1 or failing local column.
+__device__ inline int potrf_item(const Ctx& cx, double* A, double* sm) {
+  const int b = cx.b;
+  double* D = sm + GemmNT32::SMEM_DOUBLES;  // (NB+1) x NB block after the engine buffers
+  int* sflag = reinterpret_cast<int*>(D + (NB + 1) * NB);
+  for (int jb = 0; jb < b; jb += NB) {
+    const int nb = min(NB, b - jb);
+    if (jb > 0) {
+      for (int r0 = jb; r0 < b; r0 += 128) {
+        GemmNT32 g;
+        g.zero();
+        const int mm = min(128, b - r0);
+        g.run(sm, A + r0, b, A + jb, b, mm, nb, jb);
+        sub_store(g, A + r0 + (size_t)jb * b, b, mm, nb, /*lower_mask=*/r0 < jb + nb, r0, jb);
+      }
+      __syncthreads();
+    }
+    load_lower_block(D, A + jb + (size_t)jb * b, b, nb);
+    const int fail = chol_diag_block(D, nb, sflag);
+    if (fail >= 0) return jb + fail;
+    for (int e = threadIdx.x; e < nb * nb; e += TF_THREADS) {
+      const int r = e % nb, c = e / nb;
+      if (r >= c) A[jb + r + (size_t)(jb + c) * b] = D[r + c * (NB + 1)];
+    }
+    row_solve(A + jb + nb + (size_t)jb * b, b, b - jb - nb, nb, D);
+    __syncthreads();
+  }
+  return -1;
+}
+
+// TRSM (DTRSM): rows [item*RB, +RB) of X <- X L^{-T}, left-looking over
+// column blocks of NB: X[:,cb] -= X[:,<cb] L[cb,<cb]^T (DMMA), then the NB x NB solve.
+__device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int item, double* sm) {
+  const int b = cx.b;
+  const int r0 = item * RB, rows = min(RB, b - r0);
+  double* D = sm + GemmNT32::SMEM_DOUBLES;
+  X += r0;
+  for (int jb = 0; jb < b; jb += NB) {
+    const int nb = min(NB, b - jb);
+    if (jb > 0) {
+      GemmNT32 g;
+      g.zero();
+      g.run(sm, X, b, L + jb, b, rows, nb, jb);
+      sub_store(g, X + (size_t)jb * b, b, rows, nb);
+    }
+    load_lower_block(D, L + jb + (size_t)jb * b, b, nb);  // (has __syncthreads)
+    row_solve(X + (size_t)jb * b, b, rows, nb, D);
+    __syncthreads();
+  }
+}
+
+// SYRK (DGSMM with i = j): lower sub-tile `item` of C -= A A^T.
+__device__ inline void syrk_item(const Ctx& cx, const double* A, double* C, int item, double* sm) {
+  const int b = cx.b;
+  int mi = 0, rem = item;
+  while (rem > mi) { rem -= mi + 1; ++mi; }
+  const int ni = rem;  // mi >= ni
+  const int m0 = mi * RB, n0 = ni * RB;
+  const int mm = min(RB, b - m0), nn = min(RB, b - n0);
+  GemmNT128 g;
+  g.zero();
+  g.run(sm, A + m0, b, A + n0, b, mm, nn, b);
+  sub_store(g, C + m0 + (size_t)n0 * b, b, mm, nn, /*lower_mask=*/mi == ni, m0, n0);
+}
+
+// GEMM (DGSMM with i > j): sub-tile `item` of C -= A B^T.
+__device__ inline void gemm_item(const Ctx& cx, const double* A, const double* B, double* C, int item,
+                                 double* sm) {
+  const int b = cx.b;
+  const int nr = ceil_div(b, RB);
+  const int mi = item % nr, ni = item / nr;
+  const int m0 = mi * RB, n0 = ni * RB;
+  const int mm = min(RB, b - m0), nn = min(RB, b - n0);
+  GemmNT128 g;
+  g.zero();
+  g.run(sm, A + m0, b, B + n0, b, mm, nn, b);
+  sub_store(g, C + m0 + (size_t)n0 * b, b, mm, nn);
+}
+
+// ====================================================================================
+// QR (C2)
+// ====================================================================================
+
+// Householder scalars (dlarfg without safmin rescaling).
+struct House {
+  double tau, beta, den;
+};
+__device__ __forceinline__ House make_house(double alpha, double ss) {
+  House h;
+  if (ss == 0.0) { h.tau = 0.0; h.beta = alpha; h.den = 1.0; return h; }
+  const double xn = sqrt(ss);
+  const double nrm = sqrt(alpha * alpha + xn * xn);
+  h.beta = (alpha >= 0.0) ? -nrm : nrm;
+  h.tau = (h.beta - alpha) / h.beta;
+  h.den = alpha - h.beta;
+  return h;
+}
+
+// Panel of DGEQRT: P is the (mp x ib) panel A[c0:b, c0:c1] (ld ldp,
+// shared or global), Ts the ib x ib T block (smem, ld ib, pre-zeroed).
+__device__ inline void geqrt_panel(double* P, int ldp, int mp, int ib, double* Ts, double* red, double* sdot) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int jj = 0; jj < ib; ++jj) {
+    double ss = 0.0;
+    for (int r = jj + 1 + tid; r < mp; r += TF_THREADS) {
+      const double x = P[r + (size_t)jj * ldp];
+      ss += x * x;
+    }
+    ss = block_sum(ss, red);
+    const double alpha = P[jj + (size_t)jj * ldp];
+    const House h = make_house(alpha, ss);
+    __syncthreads();
+    if (ss != 0.0) {
+      for (int r = jj + 1 + tid; r < mp; r += TF_THREADS) P[r + (size_t)jj * ldp] = P[r + (size_t)jj * ldp] / h.den;
+      if (tid == 0) P[jj + (size_t)jj * ldp] = h.beta;
+    }
+    __syncthreads();
+    for (int c = warp; c < ib; c += TF_WARPS) {
+      if (c == jj) continue;
+      double s = 0.0;
+      for (int r = jj + 1 + lane; r < mp; r += 32) s += P[r + (size_t)jj * ldp] * P[r + (size_t)c * ldp];
+      s = warp_sum(s);
+      if (lane == 0) sdot[c] = P[jj + (size_t)c * ldp] + s;
+    }
+    __syncthreads();
+    const int nr = mp - jj, ncol = ib - jj - 1;
+    for (int e = tid; e < nr * ncol; e += TF_THREADS) {
+      const int r = jj + e % nr, c = jj + 1 + e / nr;
+      const double tw = h.tau * sdot[c];
+      if (r == jj) P[jj + (size_t)c * ldp] -= tw;
+      else P[r + (size_t)c * ldp] -= tw * P[r + (size_t)jj * ldp];
+    }
+    if (tid < jj) {
+      double s = 0.0;
+      for (int m = tid; m < jj; ++m) s += Ts[tid + m * ib] * (-h.tau * sdot[m]);
+      Ts[tid + jj * ib] = s;
+    }
+    if (tid == 0) Ts[jj + jj * ib] = h.tau;
+    __syncthreads();
+  }
+}
+
+// GEQRT with inner block ib.  Writes the explicit unit-lower copy of
+// V (VX, b x b) for the LARFB items of this step.
+__device__ inline void geqrt_item(const Ctx& cx, double* A, double* Tst, double* VX, double* sm) {
+  const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
+  double* W = cx.scratch;
+  double* W2 = W + (size_t)ib * b;
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    const int c1 = c0 + ib, mp = b - c0;
+    const bool in_smem = (size_t)mp * ib + (size_t)ib * ib + 2 * TF_WARPS + ib <= SMEM_DOUBLES;
+    double* Ts = sm;
+    double* red = Ts + ib * ib;
+    double* sdot = red + TF_WARPS;
+    double* P = sdot + ib + TF_WARPS;
+    int ldp = mp;
+    for (int e = tid; e < ib * ib; e += TF_THREADS) Ts[e] = 0.0;
+    if (in_smem) {
+      for (int e = tid; e < mp * ib; e += TF_THREADS) {
+        const int r = e % mp, c = e / mp;
+        P[e] = ldg_cg(A + c0 + r + (size_t)(c0 + c) * b);
+      }
+    } else {
+      P = A + c0 + (size_t)c0 * b;
+      ldp = b;
+    }
+    __syncthreads();
+    geqrt_panel(P, ldp, mp, ib, Ts, red, sdot);
+    if (in_smem) {
+      for (int e = tid; e < mp * ib; e += TF_THREADS) {
+        const int r = e % mp, c = e / mp;
+        A[c0 + r + (size_t)(c0 + c) * b] = P[e];
+      }
+    }
+    for (int e = tid; e < ib * ib; e += TF_THREADS) Tst[(size_t)c0 * ib + e] = Ts[e];
+    for (int e = tid; e < mp * ib; e += TF_THREADS) {
+      const int r = e % mp, m = e / mp;  // tile row c0 + r, column c0 + m
+      const double v = (r < m) ? 0.0 : (r == m ? 1.0 : P[r + (size_t)m * ldp]);
+      VX[c0 + r + (size_t)(c0 + m) * b] = v;
+    }
+    __syncthreads();
+    if (c1 < b) {
+      // W = V_s^T A[c0:b, c1:b];  W2 = T_s^T W;  A[c0:b, c1:b] -= V_s W2
+      w_product(sm, W, ib, VX + c0 + (size_t)c0 * b, b, A + c0 + (size_t)c1 * b, b, ib, b - c1, mp, nullptr, 0);
+      double* sT = sm;
+      load_ts(sT, Tst, ib, c0);
+      apply_tt(sT, ib, W, W2, ib, b - c1);
+      update_mn(sm, A + c0 + (size_t)c1 * b, b, VX + c0 + (size_t)c0 * b, b, W2, ib, mp, b - c1, ib);
+      __syncthreads();
+    }
+  }
+}
+
+// LARFB: slab `item` of C <- Q_kk^T C, s = 0..t-1 (reading Z5).
+__device__ inline void larfb_item(const Ctx& cx, const double* VX, const double* Tst, double* C, int item,
+                                  double* sm) {
+  const int b = cx.b, ib = cx.ib;
+  const int n0 = item * NS, nc = min(NS, b - n0);
+  double* W = cx.scratch;
+  double* W2 = W + (size_t)ib * b;
+  C += (size_t)n0 * b;
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    const int mp = b - c0;
+    w_product(sm, W, ib, VX + c0 + (size_t)c0 * b, b, C + c0, b, ib, nc, mp, nullptr, 0);
+    load_ts(sm, Tst, ib, c0);
+    apply_tt(sm, ib, W, W2, ib, nc);
+    update_mn(sm, C + c0, b, VX + c0 + (size_t)c0 * b, b, W2, ib, mp, nc, ib);
+    __syncthreads();
+  }
+}
+
+// Panel of DTSQRT: bottom P (b x ib, ld ldp), top Rb (ib x ib, ld ib,
+// upper triangle = R[c0:c1, c0:c1]), T block Ts (ld ib, pre-zeroed).
+__device__ inline void tsqrt_panel(double* P, int ldp, int b, double* Rb, int ib, double* Ts, double* red,
+                                   double* sdot) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int jj = 0; jj < ib; ++jj) {
+    double ss = 0.0;
+    for (int r = tid; r < b; r += TF_THREADS) {
+      const double x = P[r + (size_t)jj * ldp];
+      ss += x * x;
+    }
+    ss = block_sum(ss, red);
+    const double alpha = Rb[jj + jj * ib];
+    const House h = make_house(alpha, ss);
+    __syncthreads();
+    if (ss != 0.0) {
+      for (int r = tid; r < b; r += TF_THREADS) P[r + (size_t)jj * ldp] = P[r + (size_t)jj * ldp] / h.den;
+      if (tid == 0) Rb[jj + jj * ib] = h.beta;
+    }
+    __syncthreads();
+    for (int c = warp; c < ib; c += TF_WARPS) {
+      if (c == jj) continue;
+      double s = 0.0;
+      for (int r = lane; r < b; r += 32) s += P[r + (size_t)jj * ldp] * P[r + (size_t)c * ldp];
+      s = warp_sum(s);
+      if (lane == 0) sdot[c] = (c > jj) ? Rb[jj + c * ib] + s : s;
+    }
+    __syncthreads();
+    const int ncol = ib - jj - 1;
+    for (int e = tid; e < b * ncol; e += TF_THREADS) {
+      const int r = e % b, c = jj + 1 + e / b;
+      P[r + (size_t)c * ldp] -= (h.tau * sdot[c]) * P[r + (size_t)jj * ldp];
+    }
+    for (int c = jj + 1 + tid; c < ib; c += TF_THREADS) Rb[jj + c * ib] -= h.tau * sdot[c];
+    if (tid < jj) {
+      double s = 0.0;
+      for (int m = tid; m < jj; ++m) s += Ts[tid + m * ib] * (-h.tau * sdot[m]);
+      Ts[tid + jj * ib] = s;
+    }
+    if (tid == 0) Ts[jj + jj * ib] = h.tau;
+    __syncthreads();
+  }
+}
+
+// TSQRT (inner blocking PAPER.md:637-647): QR of [R; A].  Reads and
+// writes only the upper region of the diagonal tile R.
+__device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* Tst, double* sm) {
+  const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
+  double* W = cx.scratch;
+  double* W2 = W + (size_t)ib * b;
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    const int c1 = c0 + ib;
+    double* Ts = sm;
+    double* Rb = Ts + ib * ib;
+    double* red = Rb + ib * ib;
+    double* sdot = red + TF_WARPS;
+    double* P = sdot + ib + TF_WARPS;
+    const bool in_smem = (size_t)b * ib + 2 * (size_t)ib * ib + 2 * TF_WARPS + ib <= SMEM_DOUBLES;
+    int ldp = b;
+    for (int e = tid; e < ib * ib; e += TF_THREADS) {
+      const int r = e % ib, c = e / ib;
+      Ts[e] = 0.0;
+      Rb[e] = (r <= c) ? ldg_cg(R + c0 + r + (size_t)(c0 + c) * b) : 0.0;
+    }
+    if (in_smem) {
+      for (int e = tid; e < b * ib; e += TF_THREADS) P[e] = ldg_cg(A + (size_t)c0 * b + e);
+    } else {
+      P = A + (size_t)c0 * b;
+    }
+    __syncthreads();
+    tsqrt_panel(P, ldp, b, Rb, ib, Ts, red, sdot);
+    if (in_smem)
+      for (int e = tid; e < b * ib; e += TF_THREADS) A[(size_t)c0 * b + e] = P[e];
+    for (int e = tid; e < ib * ib; e += TF_THREADS) {
+      const int r = e % ib, c = e / ib;
+      if (r <= c) R[c0 + r + (size_t)(c0 + c) * b] = Rb[e];
+      Tst[(size_t)c0 * ib + e] = Ts[e];
+    }
+    __syncthreads();
+    if (c1 < b) {
+      // W = R[c0:c1, c1:b] + V_s^T A[:, c1:b]; W2 = T_s^T W; R -= W2; A[:, c1:b] -= V_s W2
+      w_product(sm, W, ib, A + (size_t)c0 * b, b, A + (size_t)c1 * b, b, ib, b - c1, b, R + c0 + (size_t)c1 * b, b);
+      load_ts(sm, Tst, ib, c0);
+      apply_tt(sm, ib, W, W2, ib, b - c1);
+      for (int e = tid; e < ib * (b - c1); e += TF_THREADS) {
+        const int m = e % ib, n = e / ib;
+        double* p = R + c0 + m + (size_t)(c1 + n) * b;
+        *p = ldg_cg(p) - W2[e];
+      }
+      update_mn(sm, A + (size_t)c1 * b, b, A + (size_t)c0 * b, b, W2, ib, b, b - c1, ib);
+      __syncthreads();
+    }
+  }
+}
+
+// SSRFB: slab `item` of [R; A] <- Q_ik^T [R; A].
+__device__ inline void ssrfb_item(const Ctx& cx, const double* V, const double* Tst, double* R, double* A,
+                                  int item, double* sm) {
+  const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
+  const int n0 = item * NS, nc = min(NS, b - n0);
+  double* W = cx.scratch;
+  double* W2 = W + (size_t)ib * b;
+  R += (size_t)n0 * b;
+  A += (size_t)n0 * b;
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    w_product(sm, W, ib, V + (size_t)c0 * b, b, A, b, ib, nc, b, R + c0, b);
+    load_ts(sm, Tst, ib, c0);
+    apply_tt(sm, ib, W, W2, ib, nc);
+    for (int e = tid; e < ib * nc; e += TF_THREADS) {
+      const int m = e % ib, n = e / ib;
+      double* p = R + c0 + m + (size_t)n * b;
+      *p = ldg_cg(p) - W2[e];
+    }
+    update_mn(sm, A, b, V + (size_t)c0 * b, b, W2, ib, b, nc, ib);
+    __syncthreads();
+  }
+}
+
+// ====================================================================================
+// LU (C3)
+// ====================================================================================
+
+// Rows c0..c0+ib of U (ld ldu) and the touched rows of A (ld lda) over columns [0, ncol):
+// apply the pairwise swaps of block (jslot[jj] >= 0: top row jj <-> A row srow[jslot]),
+// then U_s <- (I + Lb)^{-1} U_s with Lb strictly lower (smem, ld ib).  Staged through
+// shared memory in column chunks; the unit-lower solve is right-looking with the rows
+// of a column split over G lanes of one warp, subtraction order m = 0..r-1 as in C3.
+__device__ inline void swap_solve(double* U, int ldu, double* A, int lda, int ib, int ncol, const int* jslot,
+                                  const int* srow, int nslot, const double* Lb, double* buf, int bufcap) {
+  const int tid = threadIdx.x;
+  int cw = 256;
+  while (cw > 8 && (ib + nslot) * cw > bufcap) cw >>= 1;
+  const int G = TF_THREADS / cw;  // lanes per column (power of two, <= 32)
+  double* sU = buf;
+  double* sA = buf + ib * cw;
+  for (int cs = 0; cs < ncol; cs += cw) {
+    const int w = min(cw, ncol - cs);
+    for (int e = tid; e < ib * w; e += TF_THREADS) {
+      const int m = e % ib, c = e / ib;
+      sU[m + c * ib] = ldg_cg(U + m + (size_t)(cs + c) * ldu);
+    }
+    for (int e = tid; e < nslot * w; e += TF_THREADS) {
+      const int s = e % nslot, c = e / nslot;
+      sA[s + c * nslot] = ldg_cg(A + srow[s] + (size_t)(cs + c) * lda);
+    }
+    __syncthreads();
+    const int c = tid / G, g = tid % G;
+    const bool act = c < w;
+    if (act && g == 0 && jslot) {
+      for (int jj = 0; jj < ib; ++jj)
+        if (jslot[jj] >= 0) {
+          double t = sU[jj + c * ib];
+          sU[jj + c * ib] = sA[jslot[jj] + c * nslot];
+          sA[jslot[jj] + c * nslot] = t;
+        }
+    }
+    for (int m = 0; m < ib; ++m) {
+      __syncwarp();  // the G lanes of a column are consecutive lanes of one warp
+      if (act) {
+        const double xm = sU[m + c * ib];
+        for (int r = m + 1 + g; r < ib; r += G) sU[r + c * ib] -= Lb[r + m * ib] * xm;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < ib * w; e += TF_THREADS) {
+      const int m = e % ib, cc = e / ib;
+      U[m + (size_t)(cs + cc) * ldu] = sU[e];
+    }
+    for (int e = tid; e < nslot * w; e += TF_THREADS) {
+      const int s = e % nslot, cc = e / nslot;
+      A[srow[s] + (size_t)(cs + cc) * lda] = sA[e];
+    }
+    __syncthreads();
+  }
+}
+
+// Build the swap slots of inner block [c0, c0+ib) from TSTRF pivots (values > b name
+// bottom row ipiv-b-1).  rowslot: smem int[b] scratch.  Returns nslot.
+__device__ inline int build_slots(const int* ipiv, int c0, int ib, int b, int* jslot, int* srow, int* rowslot,
+                                  int* snslot) {
+  for (int r = threadIdx.x; r < b; r += TF_THREADS) rowslot[r] = -1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int ns = 0;
+    for (int jj = 0; jj < ib; ++jj) {
+      const int pv = ipiv[c0 + jj];
+      if (pv > b) {
+        const int r = pv - b - 1;
+        if (rowslot[r] < 0) { rowslot[r] = ns; srow[ns++] = r; }
+        jslot[jj] = rowslot[r];
+      } else {
+        jslot[jj] = -1;
+      }
+    }
+    *snslot = ns;
+  }
+  __syncthreads();
+  return *snslot;
+}
+
+// GETRF: LAPACK dgetrf semantics with block ib, whole-tile-row swaps
+// (Z12), first-max pivot (Z11).  Writes LX (explicit unit-lower copy of L_kk) for the
+// GESSM items.  Returns the first zero-pivot local column or -1.
+__device__ inline int getrf_item(const Ctx& cx, double* A, int* ipiv, double* LX, double* sm) {
+  const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
+  double* redv = sm;
+  int* redi = reinterpret_cast<int*>(redv + TF_WARPS);
+  int first_zero = -1;
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    const int c1 = c0 + ib;
+    for (int j = c0; j < c1; ++j) {
+      double v = -1.0;
+      int idx = INT_MAX;
+      for (int r = j + tid; r < b; r += TF_THREADS) amax_merge(v, idx, fabs(A[r + (size_t)j * b]), r);
+      const int pr = block_amax(v, idx, redv, redi);
+      const double pv = A[pr + (size_t)j * b];
+      __syncthreads();
+      if (tid == 0) ipiv[j] = pr + 1;
+      if (pv != 0.0) {
+        if (pr != j)
+          for (int c = tid; c < b; c += TF_THREADS) {
+            const double t = A[j + (size_t)c * b];
+            A[j + (size_t)c * b] = A[pr + (size_t)c * b];
+            A[pr + (size_t)c * b] = t;
+          }
+        __syncthreads();
+        const double ajj = A[j + (size_t)j * b];
+        for (int r = j + 1 + tid; r < b; r += TF_THREADS) A[r + (size_t)j * b] = A[r + (size_t)j * b] / ajj;
+      } else if (first_zero < 0) {
+        first_zero = j;
+      }
+      __syncthreads();
+      const int nr = b - j - 1, ncol = c1 - j - 1;
+      for (int e = tid; e < nr * ncol; e += TF_THREADS) {
+        const int r = j + 1 + e % nr, c = j + 1 + e / nr;
+        A[r + (size_t)c * b] -= A[r + (size_t)j * b] * A[j + (size_t)c * b];
+      }
+      __syncthreads();
+    }
+    if (c1 < b) {
+      // A[c0:c1, c1:b] <- L_ss^{-1} A[c0:c1, c1:b];  A[c1:b, c1:b] -= A[c1:b, c0:c1] A[c0:c1, c1:b]
+      double* Lb = sm;
+      double* buf = Lb + ib * ib;
+      for (int e = tid; e < ib * ib; e += TF_THREADS) {
+        const int r = e % ib, c = e / ib;
+        Lb[e] = (r > c) ? A[c0 + r + (size_t)(c0 + c) * b] : 0.0;
+      }
+      __syncthreads();
+      swap_solve(A + c0 + (size_t)c1 * b, b, nullptr, b, ib, b - c1, nullptr, nullptr, 0, Lb, buf,
+                 SMEM_DOUBLES - ib * ib - 64);
+      update_mn(sm, A + c1 + (size_t)c1 * b, b, A + c1 + (size_t)c0 * b, b, A + c0 + (size_t)c1 * b, b, b - c1,
+                b - c1, ib);
+      __syncthreads();
+    }
+  }
+  for (int e = tid; e < b * b; e += TF_THREADS) {
+    const int r = e % b, c = e / b;
+    LX[e] = (r > c) ? A[e] : (r == c ? 1.0 : 0.0);
+  }
+  return first_zero;
+}
+
+// GESSM: slab `item` of A_kj <- L_kk^{-1} P_kk A_kj.
+__device__ inline void gessm_item(const Ctx& cx, const double* LX, const int* ipiv, double* C, int item,
+                                  double* sm) {
+  const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
+  const int n0 = item * NS, nc = min(NS, b - n0);
+  C += (size_t)n0 * b;
+  // 1. P_kk: compose the b sequential interchanges into a gather permutation
+  int* perm = reinterpret_cast<int*>(sm);
+  double* buf = sm + (b + 1) / 2 + 1;
+  for (int r = tid; r < b; r += TF_THREADS) perm[r] = r;
+  __syncthreads();
+  if (tid == 0)
+    for (int j = 0; j < b; ++j) {
+      const int r = ipiv[j] - 1;
+      const int t = perm[j]; perm[j] = perm[r]; perm[r] = t;
+    }
+  __syncthreads();
+  const int cap = SMEM_DOUBLES - (b + 1) / 2 - 8;
+  const int cw = max(1, min(nc, cap / b));
+  for (int cs = 0; cs < nc; cs += cw) {
+    const int w = min(cw, nc - cs);
+    for (int e = tid; e < b * w; e += TF_THREADS) buf[e] = ldg_cg(C + (size_t)cs * b + e);
+    __syncthreads();
+    for (int e = tid; e < b * w; e += TF_THREADS) {
+      const int r = e % b, c = e / b;
+      C[(size_t)cs * b + e] = buf[perm[r] + c * b];
+    }
+    __syncthreads();
+  }
+  // 2. blocked unit-lower forward solve
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    const int c1 = c0 + ib;
+    double* Lb = sm;
+    for (int e = tid; e < ib * ib; e += TF_THREADS) {
+      const int r = e % ib, c = e / ib;
+      Lb[e] = (r > c) ? ldg_cg(LX + c0 + r + (size_t)(c0 + c) * b) : 0.0;
+    }
+    __syncthreads();
+    swap_solve(C + c0, b, nullptr, b, ib, nc, nullptr, nullptr, 0, Lb, sm + ib * ib, SMEM_DOUBLES - ib * ib - 64);
+    if (c1 < b) update_mn(sm, C + c1, b, LX + c1 + (size_t)c0 * b, b, C + c0, b, b - c1, nc, ib);
+    __syncthreads();
+  }
+}
+
+// Panel of DTSTRF (footnote PAPER.md:542-544): bottom P (b x ib, ld
+// ldp), top Ub (ib x ib, ld ib, upper = U[c0:c1, c0:c1]), L-strip block Lsb (ld ib,
+// zeroed), pivots piv[0..ib) (global, 1-based in [1, 2b]).  Returns first zero column.
+__device__ inline int tstrf_panel(double* P, int ldp, int b, double* Ub, double* Lsb, int ib, int c0, int* piv,
+                                  double* redv, int* redi) {
+  const int tid = threadIdx.x;
+  int first_zero = -1;
+  for (int jj = 0; jj < ib; ++jj) {
+    double v = -1.0;
+    int idx = INT_MAX;
+    if (tid == 0) { v = fabs(Ub[jj + jj * ib]); idx = -1; }
+    for (int r = tid; r < b; r += TF_THREADS) amax_merge(v, idx, fabs(P[r + (size_t)jj * ldp]), r);
+    const int pr = block_amax(v, idx, redv, redi);
+    if (pr >= 0) {
+      for (int c = jj + tid; c < ib; c += TF_THREADS) {
+        const double t = Ub[jj + c * ib];
+        Ub[jj + c * ib] = P[pr + (size_t)c * ldp];
+        P[pr + (size_t)c * ldp] = t;
+      }
+      for (int c = tid; c < jj; c += TF_THREADS) {
+        const double t = Lsb[jj + c * ib];
+        Lsb[jj + c * ib] = P[pr + (size_t)c * ldp];
+        P[pr + (size_t)c * ldp] = t;
+      }
+    }
+    if (tid == 0) piv[jj] = (pr >= 0) ? (b + pr + 1) : (c0 + jj + 1);
+    __syncthreads();
+    const double u = Ub[jj + jj * ib];
+    if (u != 0.0) {
+      for (int r = tid; r < b; r += TF_THREADS) P[r + (size_t)jj * ldp] = P[r + (size_t)jj * ldp] / u;
+      __syncthreads();
+      const int ncol = ib - jj - 1;
+      for (int e = tid; e < b * ncol; e += TF_THREADS) {
+        const int r = e % b, c = jj + 1 + e / b;
+        P[r + (size_t)c * ldp] -= P[r + (size_t)jj * ldp] * Ub[jj + c * ib];
+      }
+    } else if (first_zero < 0) {
+      first_zero = jj;
+    }
+    __syncthreads();
+  }
+  return first_zero;
+}
+
+// TSTRF: pairwise-pivoted LU of [U; A] (upper region of U only).
+__device__ inline int tstrf_item(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, double* sm) {
+  const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
+  int first_zero = -1;
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    const int c1 = c0 + ib;
+    double* Ub = sm;
+    double* Lsb = Ub + ib * ib;
+    double* redv = Lsb + ib * ib;
+    int* redi = reinterpret_cast<int*>(redv + TF_WARPS);
+    double* P = redv + 2 * TF_WARPS;
+    const bool in_smem = (size_t)b * ib + 2 * (size_t)ib * ib + 2 * TF_WARPS <= SMEM_DOUBLES;
+    for (int e = tid; e < ib * ib; e += TF_THREADS) {
+      const int r = e % ib, c = e / ib;
+      Ub[e] = (r <= c) ? ldg_cg(U + c0 + r + (size_t)(c0 + c) * b) : 0.0;
+      Lsb[e] = 0.0;
+    }
+    if (in_smem) {
+      for (int e = tid; e < b * ib; e += TF_THREADS) P[e] = ldg_cg(A + (size_t)c0 * b + e);
+    } else {
+      P = A + (size_t)c0 * b;
+    }
+    __syncthreads();
+    const int fz = tstrf_panel(P, b, b, Ub, Lsb, ib, c0, ipiv + c0, redv, redi);
+    if (fz >= 0 && first_zero < 0) first_zero = c0 + fz;
+    if (in_smem)
+      for (int e = tid; e < b * ib; e += TF_THREADS) A[(size_t)c0 * b + e] = P[e];
+    for (int e = tid; e < ib * ib; e += TF_THREADS) {
+      const int r = e % ib, c = e / ib;
+      if (r <= c) U[c0 + r + (size_t)(c0 + c) * b] = Ub[e];
+      Ls[(size_t)c0 * ib + e] = Lsb[e];
+    }
+    __syncthreads();
+    if (c1 < b) {
+      // stage Lb = Lsb (strictly lower) at the front of smem, then swaps + (I+Ls)^{-1}
+      double* Lb = sm;
+      for (int e = tid; e < ib * ib; e += TF_THREADS) Lb[e] = ldg_cg(Ls + (size_t)c0 * ib + e);
+      int* jslot = reinterpret_cast<int*>(Lb + ib * ib);
+      int* srow = jslot + ib;
+      int* snslot = srow + ib;
+      int* rowslot = snslot + 2;
+      __syncthreads();
+      const int nslot = build_slots(ipiv, c0, ib, b, jslot, srow, rowslot, snslot);
+      double* buf = Lb + ib * ib + (2 * ib + 2 + b + 1) / 2 + 2;
+      const int cap = SMEM_DOUBLES - (int)(buf - sm);
+      swap_solve(U + c0 + (size_t)c1 * b, b, A + (size_t)c1 * b, b, ib, b - c1, jslot, srow, nslot, Lb, buf, cap);
+      update_mn(sm, A + (size_t)c1 * b, b, A + (size_t)c0 * b, b, U + c0 + (size_t)c1 * b, b, b, b - c1, ib);
+      __syncthreads();
+    }
+  }
+  return first_zero;
+}
+
+// SSSSM: slab `item` of [U; A] <- L_ik^{-1} P_ik [U; A].
+__device__ inline void ssssm_item(const Ctx& cx, const double* L, const double* Ls, const int* ipiv, double* U,
+                                  double* A, int item, double* sm) {
+  const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
+  const int n0 = item * NS, nc = min(NS, b - n0);
+  U += (size_t)n0 * b;
+  A += (size_t)n0 * b;
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    double* Lb = sm;
+    for (int e = tid; e < ib * ib; e += TF_THREADS) Lb[e] = ldg_cg(Ls + (size_t)c0 * ib + e);
+    int* jslot = reinterpret_cast<int*>(Lb + ib * ib);
+    int* srow = jslot + ib;
+    int* snslot = srow + ib;
+    int* rowslot = snslot + 2;
+    __syncthreads();
+    const int nslot = build_slots(ipiv, c0, ib, b, jslot, srow, rowslot, snslot);
+    double* buf = Lb + ib * ib + (2 * ib + 2 + b + 1) / 2 + 2;
+    const int cap = SMEM_DOUBLES - (int)(buf - sm);
+    swap_solve(U + c0, b, A, b, ib, nc, jslot, srow, nslot, Lb, buf, cap);
+    update_mn(sm, A, b, L + (size_t)c0 * b, b, U + c0, b, b, nc, ib);
+    __syncthreads();
+  }
+}
+
+}  // namespace tf

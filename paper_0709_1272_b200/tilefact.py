@@ -1,0 +1,211 @@
+"""ctypes binding of libtilefact.so — same names as the C-ABI in include/tilefact.h.
+
+Argument marshalling only: every step of a factorization runs in the library's CUDA
+kernels.  torch is used for device memory and streams.  There is no CPU fallback: if
+the shared library is missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtilefact.so")
+
+KINDS = {"potrf": 0, "trsm": 1, "syrk": 2, "gemm": 3, "geqrt": 4, "larfb": 5, "tsqrt": 6,
+         "ssrfb": 7, "getrf": 8, "gessm": 9, "tstrf": 10, "ssssm": 11}
+KIND_NAMES = {v: k for k, v in KINDS.items()}
+ALGS = {"chol": 0, "qr": 1, "lu": 2}
+
+
+class TileFactError(RuntimeError):
+    pass
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise TileFactError(f"{LIB_PATH} is missing: run `python -m paper_0709_1272_b200.build` "
+                            "(there is no fallback path)")
+    L = ctypes.CDLL(LIB_PATH)
+    i64, i32, vp, sz = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t
+    sig = {
+        "tile_chol": (i32, [i64, i64, i64, vp, vp, vp]),
+        "tile_qr": (i32, [i64, i64, i64, vp, vp, vp]),
+        "tile_lu": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),
+        "tile_qr_t_elems": (sz, [i64, i64, i64]),
+        "tile_lu_l_elems": (sz, [i64, i64, i64]),
+        "tile_lu_ipiv_elems": (sz, [i64, i64]),
+        "tile_pack": (i32, [i64, i64, i64, vp, vp, vp]),
+        "tile_unpack": (i32, [i64, i64, i64, vp, vp, vp]),
+        "tile_factor_host": (i32, [i32, i64, i64, i64, vp, vp, vp, vp, vp]),
+        "tile_set_policy": (None, [i32]),
+        "tile_set_trace": (None, [i64]),
+        "tile_trace_fetch": (i64, [vp, i64]),
+        "tile_set_ctas": (None, [i32]),
+        "tile_dag_export": (i64, [i32, i64, i32, vp, vp, vp, vp, vp, i64, vp, vp, i64, vp]),
+        "tk_run": (i32, [i32, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
+        "tile_chol_dist": (i32, [i64, i64, i64, i32, i32, vp, vp, vp, vp]),
+        "tile_dist_local_tiles": (i64, [i64, i64, i32, i32, i32, i32]),
+        "tile_nccl_id_bytes": (i32, []),
+        "tile_nccl_get_unique_id": (i32, [vp]),
+        "tile_nccl_comm_init": (i32, [vp, i32, i32, vp]),
+        "tile_nccl_comm_destroy": (i32, [vp]),
+        "tile_strerror": (ctypes.c_char_p, [i32]),
+        "tile_last_error": (ctypes.c_char_p, []),
+        "tile_finalize": (None, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+lib = _load()
+SYMBOLS = [
+    "tile_chol", "tile_qr", "tile_lu", "tile_qr_t_elems", "tile_lu_l_elems", "tile_lu_ipiv_elems",
+    "tile_pack", "tile_unpack", "tile_factor_host", "tile_set_policy", "tile_set_trace",
+    "tile_trace_fetch", "tile_set_ctas", "tile_dag_export", "tk_run", "tile_chol_dist",
+    "tile_dist_local_tiles", "tile_nccl_id_bytes", "tile_nccl_get_unique_id", "tile_nccl_comm_init",
+    "tile_nccl_comm_destroy", "tile_strerror", "tile_last_error", "tile_finalize",
+]
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise TileFactError(f"{what} failed: rc={rc} ({lib.tile_strerror(rc).decode()}): "
+                            f"{lib.tile_last_error().decode()}")
+
+
+def _dev_f64(t, name):
+    import torch
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise TileFactError(f"{name} must be a contiguous float64 CUDA tensor")
+
+
+# ------------------------------------------------------------------ factorizations
+
+def tile_chol(n, b, ib, A, info=None, stream=None) -> None:
+    """In-place tiled Cholesky of the BDL matrix A (n*n doubles on the device)."""
+    _dev_f64(A, "A")
+    _check(lib.tile_chol(n, b, ib, _ptr(A), _ptr(info), _stream(stream)), "tile_chol")
+
+
+def tile_qr(n, b, ib, A, T, stream=None) -> None:
+    _dev_f64(A, "A")
+    _dev_f64(T, "T")
+    _check(lib.tile_qr(n, b, ib, _ptr(A), _ptr(T), _stream(stream)), "tile_qr")
+
+
+def tile_lu(n, b, ib, A, Ls, ipiv, info=None, stream=None) -> None:
+    _dev_f64(A, "A")
+    _dev_f64(Ls, "Ls")
+    _check(lib.tile_lu(n, b, ib, _ptr(A), _ptr(Ls), _ptr(ipiv), _ptr(info), _stream(stream)), "tile_lu")
+
+
+def tile_qr_t_elems(n, b, ib) -> int:
+    return int(lib.tile_qr_t_elems(n, b, ib))
+
+
+def tile_lu_l_elems(n, b, ib) -> int:
+    return int(lib.tile_lu_l_elems(n, b, ib))
+
+
+def tile_lu_ipiv_elems(n, b) -> int:
+    return int(lib.tile_lu_ipiv_elems(n, b))
+
+
+def tile_pack(m, n, b, dense, tiles, stream=None) -> None:
+    """dense: device float64 holding a column-major m x n matrix (e.g. torch tensor of
+    shape (n, m) in row-major = column-major (m, n))."""
+    _check(lib.tile_pack(m, n, b, _ptr(dense), _ptr(tiles), _stream(stream)), "tile_pack")
+
+
+def tile_unpack(m, n, b, tiles, dense, stream=None) -> None:
+    _check(lib.tile_unpack(m, n, b, _ptr(tiles), _ptr(dense), _stream(stream)), "tile_unpack")
+
+
+def tile_factor_host(kind, n, b, ib, hA, hAux=None, hIpiv=None, hInfo=None, stream=None) -> None:
+    """End-to-end host-buffer path: hA etc. are CPU tensors (pinned for speed)."""
+    k = ALGS[kind] if isinstance(kind, str) else int(kind)
+    _check(lib.tile_factor_host(k, n, b, ib, _ptr(hA), _ptr(hAux), _ptr(hIpiv), _ptr(hInfo), _stream(stream)),
+           "tile_factor_host")
+
+
+def tile_set_policy(policy: int) -> None:
+    lib.tile_set_policy(int(policy))
+
+
+def tile_set_trace(cap: int) -> None:
+    lib.tile_set_trace(int(cap))
+
+
+def tile_set_ctas(ctas: int) -> None:
+    lib.tile_set_ctas(int(ctas))
+
+
+def tile_trace_fetch(cap: int = 1 << 24):
+    """Records of the last factorization: array (N, 5) of task, item, sm, start_ns, end_ns."""
+    import numpy as np
+    buf = np.zeros((cap, 5), dtype=np.int64)
+    got = lib.tile_trace_fetch(ctypes.c_void_p(buf.ctypes.data), cap)
+    if got < 0:
+        raise TileFactError("tile_trace_fetch failed")
+    return buf[:got]
+
+
+def tile_dag_export(alg, p, policy=1):
+    """Host-only: the task graph of Algorithm 1/2/3 for p x p tiles."""
+    import numpy as np
+    a = ALGS[alg] if isinstance(alg, str) else int(alg)
+    ne = ctypes.c_int64(0)
+    nt = lib.tile_dag_export(a, p, policy, None, None, None, None, None, 0, None, None, 0, ctypes.byref(ne))
+    if nt < 0:
+        raise TileFactError("tile_dag_export failed")
+    cols = {k: np.zeros(nt, dtype=np.int32) for k in ("kind", "k", "i", "j", "level")}
+    off = np.zeros(nt + 1, dtype=np.int64)
+    succ = np.zeros(max(1, ne.value), dtype=np.int32)
+    P = lambda x: ctypes.c_void_p(x.ctypes.data)  # noqa: E731
+    lib.tile_dag_export(a, p, policy, P(cols["kind"]), P(cols["k"]), P(cols["i"]), P(cols["j"]),
+                        P(cols["level"]), nt, P(off), P(succ), ne.value, ctypes.byref(ne))
+    cols["succ_off"] = off
+    cols["succ"] = succ[:ne.value]
+    return cols
+
+
+def tk_run(kind, b, ib, t0=None, t1=None, t2=None, aux=None, ipiv=None, info=None, stream=None) -> None:
+    k = KINDS[kind] if isinstance(kind, str) else int(kind)
+    _check(lib.tk_run(k, b, ib, _ptr(t0), _ptr(t1), _ptr(t2), _ptr(aux), _ptr(ipiv), _ptr(info), _stream(stream)),
+           f"tk_run({kind})")
+
+
+def tile_finalize() -> None:
+    lib.tile_finalize()
+
+
+# ------------------------------------------------------------------ flop counts
+
+def lapack_flops(alg: str, n: int) -> float:
+    """The paper's GFLOP/s convention: LAPACK counts n^3/3, 4n^3/3, 2n^3/3."""
+    return {"chol": n ** 3 / 3.0, "qr": 4.0 * n ** 3 / 3.0, "lu": 2.0 * n ** 3 / 3.0}[alg]
+
+
+def true_flops(alg: str, n: int, b: int, ib: int) -> float:
+    """Leading-order tiled counts: x(1+ib/4b) for QR, x(1+ib/2b) for LU."""
+    f = lapack_flops(alg, n)
+    if alg == "qr":
+        return f * (1 + ib / (4.0 * b))
+    if alg == "lu":
+        return f * (1 + ib / (2.0 * b))
+    return f

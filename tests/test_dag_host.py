@@ -1,0 +1,279 @@
+"""Host-logic tests of the product's task graph (tile_dag_export; SURVEY §8(a) a13;
+PAPER.md:972-1009) and of the C-ABI surface — no GPU needed.
+
+The graph is pinned against (i) closed-form task counts, (ii) an independent generic
+RAW/WAR/WAW analysis of the algorithms' read/write sets written here, (iii) the paper's
+ready set after the first panel, (iv) the critical-path length 3p-2,
+(v) the recursive-subgraph property, and (vi) dependency soundness:
+executing the oracle's tile kernels in random topological orders of the exported graph
+reproduces the sequential oracle bitwise.
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import tilegen
+from paper_0709_1272_b200 import tilefact as tf
+
+K = tf.KINDS
+
+
+def _tasks(d):
+    return [(int(a), int(b), int(c), int(e)) for a, b, c, e in zip(d["kind"], d["k"], d["i"], d["j"])]
+
+
+def _preds(d):
+    nt = len(d["kind"])
+    pr = [set() for _ in range(nt)]
+    for t in range(nt):
+        for e in range(d["succ_off"][t], d["succ_off"][t + 1]):
+            pr[int(d["succ"][e])].add(t)
+    return pr
+
+
+def _rw(alg, kind, k, i, j):
+    """Read / write regions of each task (diagonal tiles split into lo / up for QR, LU)."""
+    if alg == "chol":
+        return {
+            K["potrf"]: ([], [("A", k, k)]),
+            K["trsm"]: ([("A", k, k)], [("A", i, k)]),
+            K["syrk"]: ([("A", i, k)], [("A", i, i)]),
+            K["gemm"]: ([("A", i, k), ("A", j, k)], [("A", i, j)]),
+        }[kind]
+    F, R, C, U = (4, 5, 6, 7) if alg == "qr" else (8, 9, 10, 11)
+
+    def whole(r, c):  # a full tile; diagonal tiles are the union of their two regions
+        return [("lo", r, r), ("up", r, r)] if r == c else [("A", r, c)]
+
+    if kind == F:
+        return [], whole(k, k) + [("X", k, k)]
+    if kind == R:
+        return [("lo", k, k), ("X", k, k)], whole(k, j)
+    if kind == C:
+        return [], [("up", k, k)] + whole(i, k) + [("X", i, k)]
+    return whole(i, k) + [("X", i, k)], whole(k, j) + whole(i, j)
+
+
+def _generic_preds(alg, tasks):
+    last_w, readers = {}, {}
+    pr = []
+    for t, (kind, k, i, j) in enumerate(tasks):
+        rd, wr = _rw(alg, kind, k, i, j)
+        p = set()
+        for r in rd + wr:
+            if r in last_w:
+                p.add(last_w[r])          # RAW / WAW
+        for r in wr:
+            p.update(readers.get(r, ()))  # WAR
+        p.discard(t)
+        for r in rd:
+            readers.setdefault(r, set()).add(t)
+        for r in wr:
+            last_w[r] = t
+            readers[r] = set()
+        pr.append(p)
+    return pr
+
+
+@pytest.mark.parametrize("alg,p,nt,ne", [("chol", 8, 120, 252), ("qr", 16, 1496, 3960), ("lu", 16, 1496, 3960),
+                                         ("qr", 3, 14, None), ("chol", 3, 10, None)])
+def test_counts(alg, p, nt, ne):
+    d = tf.tile_dag_export(alg, p)
+    assert len(d["kind"]) == nt
+    if ne is not None:
+        assert len(d["succ"]) == ne
+    if alg == "chol":
+        assert nt == p + p * (p - 1) + p * (p - 1) * (p - 2) // 6
+    else:
+        assert nt == p + p * (p - 1) + (p - 1) * p * (2 * p - 1) // 6
+
+
+@pytest.mark.slow
+def test_counts_large():
+    assert len(tf.tile_dag_export("chol", 64)["succ"]) == 131040
+    assert len(tf.tile_dag_export("qr", 64)["succ"]) == 260064
+
+
+@pytest.mark.parametrize("alg,p", [("chol", 1), ("chol", 5), ("chol", 8), ("qr", 1), ("qr", 4), ("qr", 9),
+                                   ("lu", 6)])
+def test_matches_generic_dependency_analysis(alg, p):
+    d = tf.tile_dag_export(alg, p)
+    tasks = _tasks(d)
+    assert _preds(d) == _generic_preds(alg, tasks)
+
+
+def test_ready_set_after_first_panel():
+    """SPEC.md:350-351 (0-based): after GEQRT(0) on p = 3: {LARFB(0,1), LARFB(0,2), TSQRT(1,0)}."""
+    d = tf.tile_dag_export("qr", 3)
+    tasks = _tasks(d)
+    pr = _preds(d)
+    roots = [t for t in range(len(tasks)) if not pr[t]]
+    assert [tasks[t] for t in roots] == [(K["geqrt"], 0, 0, 0)]
+    done = {roots[0]}
+    ready = {tasks[t] for t in range(len(tasks)) if t not in done and pr[t] <= done}
+    assert ready == {(K["larfb"], 0, 0, 1), (K["larfb"], 0, 0, 2), (K["tsqrt"], 0, 1, 0)}
+
+
+@pytest.mark.parametrize("alg,p", [("chol", 8), ("qr", 16), ("lu", 7), ("chol", 1)])
+def test_critical_path(alg, p):
+    d = tf.tile_dag_export(alg, p)
+    pr = _preds(d)
+    depth = [1] * len(pr)
+    for t in range(len(pr)):  # program order is a topological order
+        if pr[t]:
+            depth[t] = 1 + max(depth[x] for x in pr[t])
+    assert max(depth) == 3 * p - 2
+
+
+def test_priorities():
+    """GEQRT > TSQRT > LARFB > SSRFB (policy 0 = the paper's ranks)."""
+    d = tf.tile_dag_export("qr", 4, policy=0)
+    lev = {int(k): set() for k in np.unique(d["kind"])}
+    for kind, l in zip(d["kind"], d["level"]):
+        lev[int(kind)].add(int(l))
+    assert lev[K["geqrt"]] == {0} and lev[K["tsqrt"]] == {1} and lev[K["larfb"]] == {2} and lev[K["ssrfb"]] == {3}
+    d = tf.tile_dag_export("chol", 4, policy=0)
+    lv = dict(zip(_tasks(d), d["level"]))
+    assert lv[(K["potrf"], 1, 1, 1)] < lv[(K["trsm"], 1, 2, 1)] < lv[(K["gemm"], 1, 3, 2)]
+    # lookahead policy: updates of the next panel column are promoted
+    d = tf.tile_dag_export("chol", 4, policy=1)
+    lv = dict(zip(_tasks(d), d["level"]))
+    assert lv[(K["gemm"], 0, 3, 1)] < lv[(K["gemm"], 0, 3, 2)]
+
+
+def test_recursive_subgraph():
+    """the DAG for p2 <= p1 is an induced subgraph of the DAG for p1."""
+    for alg in ("chol", "qr"):
+        small, big = tf.tile_dag_export(alg, 4), tf.tile_dag_export(alg, 7)
+        ts, tb = _tasks(small), _tasks(big)
+        idx = {t: n for n, t in enumerate(tb)}
+        ps, pb = _preds(small), _preds(big)
+        for n, t in enumerate(ts):
+            assert t in idx
+            assert {ts[x] for x in ps[n]} == {tb[x] for x in pb[idx[t]] if tb[x] in set(ts)}
+
+
+# ------------------------------------------------------------------ dependency soundness
+
+def _run_task(alg, F, X, piv, p, b, ib, task):
+    kind, k, i, j = task
+    bb = b * b
+
+    def T(r, c):
+        return F[(r + c * p) * bb:(r + c * p + 1) * bb].reshape(b, b).T  # view, (row, col)
+
+    def S(r, c):
+        o = (r + c * p) * ib * b
+        return X[o:o + ib * b].reshape(b, ib).T
+
+    def PV(r, c):
+        o = (r + c * p) * b
+        return piv[o:o + b]
+
+    def f(a):  # column-major view the oracle can write through
+        return np.asfortranarray(a)
+
+    # Each oracle call operates on Fortran views aliasing F / X (T(...) is a transposed
+    # view of a C-contiguous block, i.e. a Fortran-contiguous matrix).
+    if kind == K["potrf"]:
+        oracle.potrf(T(k, k))
+    elif kind == K["trsm"]:
+        oracle.trsm(T(k, k), T(i, k))
+    elif kind == K["syrk"]:
+        oracle.syrk(T(i, k), T(i, i))
+    elif kind == K["gemm"]:
+        oracle.gemm_nt(T(i, k), T(j, k), T(i, j))
+    elif kind == K["geqrt"]:
+        S(k, k)[:] = oracle.geqrt(T(k, k), ib)
+    elif kind == K["larfb"]:
+        oracle.larfb(T(k, k), f(S(k, k)), T(k, j), ib)
+    elif kind == K["tsqrt"]:
+        S(i, k)[:] = oracle.tsqrt(T(k, k), T(i, k), ib)
+    elif kind == K["ssrfb"]:
+        oracle.ssrfb(T(i, k), f(S(i, k)), T(k, j), T(i, j), ib)
+    elif kind == K["getrf"]:
+        pv, _ = oracle.getrf(T(k, k), ib)
+        PV(k, k)[:] = pv
+    elif kind == K["gessm"]:
+        oracle.gessm(T(k, k), np.ascontiguousarray(PV(k, k)), T(k, j), ib)
+    elif kind == K["tstrf"]:
+        ls, pv, _ = oracle.tstrf(T(k, k), T(i, k), ib)
+        S(i, k)[:] = ls
+        PV(i, k)[:] = pv
+    elif kind == K["ssssm"]:
+        oracle.ssssm(T(i, k), f(S(i, k)), np.ascontiguousarray(PV(i, k)), T(k, j), T(i, j), ib)
+
+
+@pytest.mark.parametrize("alg", ["chol", "qr", "lu"])
+def test_random_topological_replay_bitwise(alg):
+    n, b, ib, p = 48, 12, 4, 4
+    A = {"chol": tilegen.spd, "qr": tilegen.uniform, "lu": tilegen.normal}[alg](n, 3)
+    ref = oracle.pack(A, b)
+    if alg == "chol":
+        oracle.chol(ref, n, b)
+        refX = None
+    elif alg == "qr":
+        refX = oracle.qr(ref, n, b, ib)
+    else:
+        refX, refP, _ = oracle.lu(ref, n, b, ib)
+    d = tf.tile_dag_export(alg, p)
+    tasks = _tasks(d)
+    pr = _preds(d)
+    rng = np.random.default_rng(0)
+    for rep in range(6):
+        F = oracle.pack(A, b)
+        X = np.zeros(p * p * ib * b)
+        piv = np.zeros(p * p * b, dtype=np.int32)
+        indeg = [len(x) for x in pr]
+        succ = [[] for _ in tasks]
+        for t, ps in enumerate(pr):
+            for x in ps:
+                succ[x].append(t)
+        ready = [t for t in range(len(tasks)) if indeg[t] == 0]
+        while ready:
+            t = ready.pop(int(rng.integers(len(ready))))
+            _run_task(alg, F, X, piv, p, b, ib, tasks[t])
+            for s in succ[t]:
+                indeg[s] -= 1
+                if indeg[s] == 0:
+                    ready.append(s)
+        assert np.array_equal(F, ref)
+        if alg == "qr":
+            assert np.array_equal(X, refX)
+        if alg == "lu":
+            assert np.array_equal(X, refX) and np.array_equal(piv, refP)
+
+
+# ------------------------------------------------------------------ C-ABI surface
+
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "tilefact.h")).read()
+    names = set(re.findall(r"^\s*(?:const\s+)?[A-Za-z_0-9]+\s*\*?\s+\**\s*(t[a-z_]+)\s*\(", hdr, re.M))
+    assert {"tile_chol", "tile_qr", "tile_lu", "tk_run", "tile_pack"} <= names
+    for nm in names:
+        assert hasattr(tf.lib, nm), nm
+    assert set(tf.SYMBOLS) == names
+
+
+def test_argument_validation_without_gpu():
+    L = tf.lib
+    vp = ctypes.c_void_p(16)
+    assert L.tile_chol(0, 4, 4, vp, None, None) == -1
+    assert L.tile_chol(10, 4, 4, vp, None, None) == -2
+    assert L.tile_chol(8, 4, 3, vp, None, None) == -3
+    assert L.tile_chol(8, 4, 4, None, None, None) == -4
+    assert L.tile_qr(8, 4, 2, vp, None, None) == -5
+    assert L.tile_lu(8, 4, 2, vp, vp, None, None, None) == -6
+    assert L.tile_qr_t_elems(4096, 256, 32) == 16 * 16 * 32 * 256
+    assert L.tile_lu_ipiv_elems(4096, 256) == 16 * 16 * 256
+    assert L.tile_strerror(-1) == b"invalid argument"
+
+
+def test_flop_conventions():
+    assert tf.lapack_flops("chol", 32768) == pytest.approx(1.1728e13, rel=1e-4)
+    assert tf.lapack_flops("qr", 32768) == pytest.approx(4.6912e13, rel=1e-4)
+    assert tf.true_flops("qr", 4096, 256, 32) / tf.lapack_flops("qr", 4096) == pytest.approx(1 + 32 / 1024)

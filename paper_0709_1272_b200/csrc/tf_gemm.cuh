@@ -1,40 +1,52 @@
 // tf_gemm.cuh — CTA-wide FP64 DMMA tile-product engine (the update kernels' core).
 //
 // acc(BM x BN) = sum_{k<K} Aop(m,k) * Bop(k,n) for one CTA tile, with
-//   Aop(m,k) at A[m + k*lda] (A_KMAJ = false, "m-contiguous") or A[k + m*lda] (true),
-//   Bop(k,n) at B[n + k*ldb] (B_KMAJ = false, "n-contiguous") or B[k + n*ldb] (true).
+//   Aop(m,k) at A[m + k*lda] (AK = false, "m-contiguous") or A[k + m*lda] (AK = true),
+//   Bop(k,n) at B[n + k*ldb] (BK = false, "n-contiguous") or B[k + n*ldb] (BK = true).
 // Rows m >= M, columns n >= N and k >= K are zero-filled, so ragged edges are exact.
 // Operands stream global -> shared through an NST-stage cp.async ring of KC-deep
-// slices; each warp owns a (BM/WM) x (BN/WN) sub-tile of m8n8k4 DMMA fragments held in
-// registers.  The caller consumes the accumulators with for_each(f(r, c, v)).
+// slices; each of the 16 warps owns a (BM/WM) x (BN/WN) tile of m8n8k4 DMMA fragments
+// in registers.  The caller consumes the accumulators with for_each(f(r, c, v)).
 //
-// Shared layouts (doubles):  m-contig A slice: [KC][BM+4]; k-major A slice: [BM][KC+4]
-// (same for B with BN).  Both paddings make the 16-lane fragment reads (4 rows x 4 k)
-// hit 16 distinct bank pairs.
+// Fragment loads are 128-bit: the MMA row / column / k labels are free (a product is
+// a sum over k, and the accumulator rows/columns are relabelled in for_each), so each
+// lane's two fragments are made adjacent in shared memory:
+//   m-contiguous A: fragments (2i', 2i'+1) of lane row r sit at m = 16 i' + 2r + {0,1};
+//   n-contiguous B: likewise over n;
+//   k-major operands: k-steps are taken in pairs, lane column q reads k = 8s + 2q + {0,1}
+//   (and then every operand uses that k labelling, KPERM).
+// Padded strides make every 8-lane phase of a 128-bit load hit 8 distinct 16-byte bank
+// groups (m/n-contiguous: stride = 4 mod 16 natural k, 2 mod 8 permuted k; k-major:
+// stride KC + 8).
 #pragma once
 #include "tf_common.cuh"
 
 namespace tf {
 
-constexpr int KC = 16;    // k-depth of one pipeline slice
-constexpr int NST = 3;    // pipeline stages
+constexpr int KC = 16;  // k-depth of one pipeline slice
+constexpr int NST = 4;  // pipeline stages
 
 template <int BM, int BN, bool AK, bool BK>
-struct GemmSmem {
-  static constexpr int A_ELEMS = AK ? BM * (KC + 4) : KC * (BM + 4);
-  static constexpr int B_ELEMS = BK ? BN * (KC + 4) : KC * (BN + 4);
-  static constexpr int STAGE = A_ELEMS + B_ELEMS;
-  static constexpr int TOTAL = NST * STAGE;  // doubles
+struct GemmLayout {
+  static constexpr bool KPERM = AK || BK;
+  static constexpr int SMN_A = BM + (KPERM ? 2 : 4);  // m-contiguous A row stride (doubles)
+  static constexpr int SMN_B = BN + (KPERM ? 2 : 4);
+  static constexpr int SK = KC + 8;                   // k-major row stride
+  static constexpr int A_ELEMS = AK ? BM * SK : KC * SMN_A;
+  static constexpr int B_ELEMS = BK ? BN * SK : KC * SMN_B;
+  static constexpr int STAGE = ((A_ELEMS + B_ELEMS + 1) / 2) * 2;  // keep 16-byte alignment
+  static constexpr int TOTAL = NST * STAGE;                        // doubles
 };
 
 template <int BM, int BN, int WM, int WN, bool AK, bool BK>
 struct Gemm {
-  static_assert(WM * WN == TF_WARPS, "8 warps");
+  static_assert(WM * WN == TF_WARPS, "all warps own a sub-tile");
   static constexpr int TM = BM / WM, TN = BN / WN;  // warp tile
   static constexpr int MI = TM / 8, NI = TN / 8;
-  static_assert(MI >= 1 && NI >= 1 && TM % 8 == 0 && TN % 8 == 0, "warp tile");
-  using S = GemmSmem<BM, BN, AK, BK>;
-  static constexpr int SMEM_DOUBLES = S::TOTAL;
+  static_assert(TM % 16 == 0 && TN % 16 == 0, "fragments come in pairs");
+  using Lay = GemmLayout<BM, BN, AK, BK>;
+  static constexpr bool KPERM = Lay::KPERM;
+  static constexpr int SMEM_DOUBLES = Lay::TOTAL;
 
   double acc[MI][NI][2];
 
@@ -45,93 +57,127 @@ struct Gemm {
       for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   }
 
-  // Issue the cp.async copies of slice `kt` into stage buffer `st`.
   template <int VEC>
   __device__ __forceinline__ static void load_slice(double* sm, int st, const double* __restrict__ A, int lda,
                                                     const double* __restrict__ B, int ldb, int M, int N, int K,
                                                     int kt) {
-    double* sA = sm + st * S::STAGE;
-    double* sB = sA + S::A_ELEMS;
+    double* sA = sm + st * Lay::STAGE;
+    double* sB = sA + Lay::A_ELEMS;
     const int k0 = kt * KC;
     const int tid = threadIdx.x;
-    // ---- A
     if (!AK) {
-      constexpr int CPR = BM / VEC;  // chunks per k-row
-      for (int c = tid; c < KC * CPR; c += TF_THREADS) {
+      constexpr int CPR = BM / VEC, TOT = KC * CPR;
+#pragma unroll
+      for (int c = tid; c < TOT; c += TF_THREADS) {
         const int k = c / CPR, m = (c % CPR) * VEC;
         const int gk = k0 + k;
         int valid = (gk < K) ? (M - m) : 0;
         valid = valid < 0 ? 0 : (valid > VEC ? VEC : valid);
         const double* src = valid ? (A + m + (size_t)gk * lda) : A;
-        double* dst = sA + k * (BM + 4) + m;
+        double* dst = sA + k * Lay::SMN_A + m;
         if (VEC == 2) cp_async16(dst, src, valid * 8); else cp_async8(dst, src, valid * 8);
       }
     } else {
-      constexpr int CPR = KC / VEC;
-      for (int c = tid; c < BM * CPR; c += TF_THREADS) {
+      constexpr int CPR = KC / VEC, TOT = BM * CPR;
+#pragma unroll
+      for (int c = tid; c < TOT; c += TF_THREADS) {
         const int m = c / CPR, k = (c % CPR) * VEC;
         const int gk = k0 + k;
         int valid = (m < M) ? (K - gk) : 0;
         valid = valid < 0 ? 0 : (valid > VEC ? VEC : valid);
         const double* src = valid ? (A + gk + (size_t)m * lda) : A;
-        double* dst = sA + m * (KC + 4) + k;
+        double* dst = sA + m * Lay::SK + k;
         if (VEC == 2) cp_async16(dst, src, valid * 8); else cp_async8(dst, src, valid * 8);
       }
     }
-    // ---- B
     if (!BK) {
-      constexpr int CPR = BN / VEC;
-      for (int c = tid; c < KC * CPR; c += TF_THREADS) {
+      constexpr int CPR = BN / VEC, TOT = KC * CPR;
+#pragma unroll
+      for (int c = tid; c < TOT; c += TF_THREADS) {
         const int k = c / CPR, n = (c % CPR) * VEC;
         const int gk = k0 + k;
         int valid = (gk < K) ? (N - n) : 0;
         valid = valid < 0 ? 0 : (valid > VEC ? VEC : valid);
         const double* src = valid ? (B + n + (size_t)gk * ldb) : B;
-        double* dst = sB + k * (BN + 4) + n;
+        double* dst = sB + k * Lay::SMN_B + n;
         if (VEC == 2) cp_async16(dst, src, valid * 8); else cp_async8(dst, src, valid * 8);
       }
     } else {
-      constexpr int CPR = KC / VEC;
-      for (int c = tid; c < BN * CPR; c += TF_THREADS) {
+      constexpr int CPR = KC / VEC, TOT = BN * CPR;
+#pragma unroll
+      for (int c = tid; c < TOT; c += TF_THREADS) {
         const int n = c / CPR, k = (c % CPR) * VEC;
         const int gk = k0 + k;
         int valid = (n < N) ? (K - gk) : 0;
         valid = valid < 0 ? 0 : (valid > VEC ? VEC : valid);
         const double* src = valid ? (B + gk + (size_t)n * ldb) : B;
-        double* dst = sB + n * (KC + 4) + k;
+        double* dst = sB + n * Lay::SK + k;
         if (VEC == 2) cp_async16(dst, src, valid * 8); else cp_async8(dst, src, valid * 8);
       }
     }
   }
 
+  // k row read by lane column q at k-step kk of a slice
+  __device__ __forceinline__ static int kidx(int kk, int q) {
+    return KPERM ? (8 * (kk >> 1) + 2 * q + (kk & 1)) : (4 * kk + q);
+  }
+
   __device__ __forceinline__ void compute_slice(const double* sm, int st) {
-    const double* sA = sm + st * S::STAGE;
-    const double* sB = sA + S::A_ELEMS;
+    const double* sA = sm + st * Lay::STAGE;
+    const double* sB = sA + Lay::A_ELEMS;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = warp / WN, wn = warp % WN;
     const int r = lane >> 2, q = lane & 3;
 #pragma unroll
-    for (int kk = 0; kk < KC; kk += 4) {
-      double a[MI], b[NI];
+    for (int s = 0; s < KC / 8; ++s) {
+      double a[2][MI], b[2][NI];  // [k-step parity][fragment]
+      // ---- k-major operands: one 128-bit load covers both k-steps of the pair
+      if (AK) {
 #pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        const int m = wm * TM + i * 8 + r;
-        a[i] = AK ? sA[m * (KC + 4) + kk + q] : sA[(kk + q) * (BM + 4) + m];
+        for (int i = 0; i < MI; ++i) {
+          const double2 v = *reinterpret_cast<const double2*>(sA + (wm * TM + 8 * i + r) * Lay::SK + 8 * s + 2 * q);
+          a[0][i] = v.x;
+          a[1][i] = v.y;
+        }
+      }
+      if (BK) {
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const double2 v = *reinterpret_cast<const double2*>(sB + (wn * TN + 8 * j + r) * Lay::SK + 8 * s + 2 * q);
+          b[0][j] = v.x;
+          b[1][j] = v.y;
+        }
       }
 #pragma unroll
-      for (int j = 0; j < NI; ++j) {
-        const int n = wn * TN + j * 8 + r;
-        b[j] = BK ? sB[n * (KC + 4) + kk + q] : sB[(kk + q) * (BN + 4) + n];
+      for (int h = 0; h < 2; ++h) {
+        const int kk = 2 * s + h;
+        const int kr = kidx(kk, q);
+        if (!AK) {
+#pragma unroll
+          for (int i2 = 0; i2 < MI / 2; ++i2) {
+            const double2 v = *reinterpret_cast<const double2*>(sA + kr * Lay::SMN_A + wm * TM + 16 * i2 + 2 * r);
+            a[h][2 * i2] = v.x;
+            a[h][2 * i2 + 1] = v.y;
+          }
+        }
+        if (!BK) {
+#pragma unroll
+          for (int j2 = 0; j2 < NI / 2; ++j2) {
+            const double2 v = *reinterpret_cast<const double2*>(sB + kr * Lay::SMN_B + wn * TN + 16 * j2 + 2 * r);
+            b[h][2 * j2] = v.x;
+            b[h][2 * j2 + 1] = v.y;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) dmma(acc[i][j], a[h][i], b[h][j]);
       }
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NI; ++j) dmma(acc[i][j], a[i], b[j]);
     }
   }
 
-  // acc += Aop(0:M, 0:K) * Bop(0:K, 0:N).  All 256 threads must call.  On return the
-  // shared buffers are free for reuse (trailing __syncthreads).
+  // acc += Aop(0:M, 0:K) * Bop(0:K, 0:N).  All threads must call.  On return the shared
+  // buffers are free for reuse (trailing __syncthreads).
   template <int VEC>
   __device__ __forceinline__ void run_v(double* sm, const double* A, int lda, const double* B, int ldb, int M,
                                         int N, int K) {
@@ -161,7 +207,7 @@ struct Gemm {
     else run_v<1>(sm, A, lda, B, ldb, M, N, K);
   }
 
-  // f(r, c, v) for every accumulator element inside [0,M) x [0,N).
+  // f(r, c, v) for every accumulator element inside [0,M) x [0,N) (undoing the labels).
   template <class F>
   __device__ __forceinline__ void for_each(int M, int N, F&& f) const {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -173,22 +219,122 @@ struct Gemm {
       for (int j = 0; j < NI; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int rr = wm * TM + i * 8 + r, cc = wn * TN + j * 8 + 2 * q + e;
+          const int rr = AK ? (wm * TM + 8 * i + r) : (wm * TM + 16 * (i >> 1) + 2 * r + (i & 1));
+          const int cl = 2 * q + e;  // local column of the C fragment = B fragment's n label
+          const int cc = BK ? (wn * TN + 8 * j + cl) : (wn * TN + 16 * (j >> 1) + 2 * cl + (j & 1));
           if (rr < M && cc < N) f(rr, cc, acc[i][j][e]);
         }
+  }
+
+  // C -= acc (see sub_store).
+  __device__ __forceinline__ void sub_from(double* C, int ldc, int M, int N, bool mask, int row0, int col0) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const int r = lane >> 2, q = lane & 3;
+    const bool vec = !AK && ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc & 1) == 0);
+    if (!vec) {
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int rr = AK ? (wm * TM + 8 * i + r) : (wm * TM + 16 * (i >> 1) + 2 * r + (i & 1));
+        double cv[NI][2];
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cl = 2 * q + e;
+            const int cc = BK ? (wn * TN + 8 * j + cl) : (wn * TN + 16 * (j >> 1) + 2 * cl + (j & 1));
+            cv[j][e] = (rr < M && cc < N) ? ldg_cg(C + rr + (size_t)cc * ldc) : 0.0;
+          }
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cl = 2 * q + e;
+            const int cc = BK ? (wn * TN + 8 * j + cl) : (wn * TN + 16 * (j >> 1) + 2 * cl + (j & 1));
+            if (rr < M && cc < N && !(mask && row0 + rr < col0 + cc)) C[rr + (size_t)cc * ldc] = cv[j][e] - acc[i][j][e];
+          }
+      }
+      return;
+    }
+#pragma unroll
+    for (int i2 = 0; i2 < MI / 2; ++i2) {
+      const int rr = wm * TM + 16 * i2 + 2 * r;  // rows rr, rr+1 <-> acc[2*i2], acc[2*i2+1]
+#pragma unroll
+      for (int jb = 0; jb < NI; jb += 2) {  // batches of 4 row pairs: loads first, then stores
+        double2 cv[2][2];
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = jb + jj, cl = 2 * q + e;
+            const int cc = BK ? (wn * TN + 8 * j + cl) : (wn * TN + 16 * (j >> 1) + 2 * cl + (j & 1));
+            const double* p = C + rr + (size_t)cc * ldc;
+            cv[jj][e].x = cv[jj][e].y = 0.0;
+            if (cc < N) {
+              if (rr + 1 < M) cv[jj][e] = __ldcg(reinterpret_cast<const double2*>(p));
+              else if (rr < M) cv[jj][e].x = __ldcg(p);
+            }
+          }
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = jb + jj, cl = 2 * q + e;
+            const int cc = BK ? (wn * TN + 8 * j + cl) : (wn * TN + 16 * (j >> 1) + 2 * cl + (j & 1));
+            if (cc >= N) continue;
+            double* p = C + rr + (size_t)cc * ldc;
+            double2 v;
+            v.x = cv[jj][e].x - acc[2 * i2][j][e];
+            v.y = cv[jj][e].y - acc[2 * i2 + 1][j][e];
+            const bool w0 = rr < M && !(mask && row0 + rr < col0 + cc);
+            const bool w1 = rr + 1 < M && !(mask && row0 + rr + 1 < col0 + cc);
+            if (w0 && w1) {
+              *reinterpret_cast<double2*>(p) = v;
+            } else {
+              if (w0) p[0] = v.x;
+              if (w1) p[1] = v.y;
+            }
+          }
+      }
+    }
+  }
+
+  // f(j, e, row, col) over the in-range elements of accumulator row-fragment i.
+  template <class F>
+  __device__ __forceinline__ void for_row(int i, int M, int N, F&& f) const {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const int r = lane >> 2, q = lane & 3;
+    const int rr = AK ? (wm * TM + 8 * i + r) : (wm * TM + 16 * (i >> 1) + 2 * r + (i & 1));
+#pragma unroll
+    for (int j = 0; j < NI; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cl = 2 * q + e;
+        const int cc = BK ? (wn * TN + 8 * j + cl) : (wn * TN + 16 * (j >> 1) + 2 * cl + (j & 1));
+        if (rr < M && cc < N) f(j, e, rr, cc);
+      }
   }
 };
 
 // C(MxN, ldc) -= acc with C in global memory (L2 path).  Optional lower mask: only
 // elements with (row0 + r) >= (col0 + c) are written (SYRK on a diagonal sub-tile).
+// For m-contiguous A the two rows of a fragment pair are adjacent in a column of C, so
+// the read-modify-write uses 128-bit accesses, with all loads of a row pair issued
+// before any store (one L2 round trip per pair instead of one per element).
 template <class G>
 __device__ __forceinline__ void sub_store(const G& g, double* C, int ldc, int M, int N, bool lower_mask = false,
                                           int row0 = 0, int col0 = 0) {
-  g.for_each(M, N, [&](int r, int c, double v) {
-    if (lower_mask && row0 + r < col0 + c) return;
-    double* p = C + r + (size_t)c * ldc;
-    *p = ldg_cg(p) - v;
-  });
+  g.sub_from(C, ldc, M, N, lower_mask, row0, col0);
+}
+
+// Warm L2 with the M x N block of C (column-major, ld ldc) ahead of its epilogue.
+__device__ __forceinline__ void prefetch_l2(const double* C, int ldc, int M, int N) {
+  const int lpc = (M * 8 + 127) / 128;  // 128-byte lines per column
+  for (int e = threadIdx.x; e < lpc * N; e += TF_THREADS) {
+    const double* p = C + (size_t)(e / lpc) * ldc + (e % lpc) * 16;
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+  }
 }
 
 }  // namespace tf

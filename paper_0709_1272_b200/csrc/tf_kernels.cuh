@@ -1,5 +1,5 @@
 // tf_kernels.cuh — the eleven tile kernels of Algorithms 1-3 as CTA-wide device
-// functions (256 threads, one work item each), called by the persistent scheduler
+// functions (512 threads, one work item each), called by the persistent scheduler
 // (tf_lib.cu) and by the per-kernel test launcher tk_run.
 //
 //   Cholesky:  POTRF, TRSM, SYRK (DGSMM i=j), GEMM (DGSMM i>j)
@@ -49,11 +49,11 @@ __host__ __device__ inline int items_of(int kind, int b) {
   }
 }
 
-using GemmNT128 = Gemm<128, 128, 2, 4, false, false>;
-using GemmNT32 = Gemm<128, 32, 4, 2, false, false>;
-using GemmW64 = Gemm<64, 64, 2, 4, true, true>;
-using GemmW32 = Gemm<32, 128, 1, 8, true, true>;
-using GemmUpd = Gemm<128, 64, 4, 2, false, true>;
+using GemmNT128 = Gemm<128, 128, 4, 4, false, false>;
+using GemmNT32 = Gemm<128, 32, 8, 2, false, false>;
+using GemmW64 = Gemm<64, 64, 4, 4, true, true>;
+using GemmW32 = Gemm<32, 128, 2, 8, true, true>;
+using GemmUpd = Gemm<128, 64, 4, 4, false, true>;
 
 // C(M x N, ldc) -= Aop * Bop over tiles of the update engine (A m-contig, B k-major).
 __device__ inline void update_mn(double* sm, double* C, int ldc, const double* A, int lda, const double* B,
@@ -236,6 +236,7 @@ __device__ inline void syrk_item(const Ctx& cx, const double* A, double* C, int 
   const int ni = rem;  // mi >= ni
   const int m0 = mi * RB, n0 = ni * RB;
   const int mm = min(RB, b - m0), nn = min(RB, b - n0);
+  prefetch_l2(C + m0 + (size_t)n0 * b, b, mm, nn);
   GemmNT128 g;
   g.zero();
   g.run(sm, A + m0, b, A + n0, b, mm, nn, b);
@@ -250,6 +251,7 @@ __device__ inline void gemm_item(const Ctx& cx, const double* A, const double* B
   const int mi = item % nr, ni = item / nr;
   const int m0 = mi * RB, n0 = ni * RB;
   const int mm = min(RB, b - m0), nn = min(RB, b - n0);
+  prefetch_l2(C + m0 + (size_t)n0 * b, b, mm, nn);
   GemmNT128 g;
   g.zero();
   g.run(sm, A + m0, b, B + n0, b, mm, nn, b);
@@ -518,8 +520,8 @@ __device__ inline void ssrfb_item(const Ctx& cx, const double* V, const double* 
 __device__ inline void swap_solve(double* U, int ldu, double* A, int lda, int ib, int ncol, const int* jslot,
                                   const int* srow, int nslot, const double* Lb, double* buf, int bufcap) {
   const int tid = threadIdx.x;
-  int cw = 256;
-  while (cw > 8 && (ib + nslot) * cw > bufcap) cw >>= 1;
+  int cw = TF_THREADS;
+  while (cw > 16 && (ib + nslot) * cw > bufcap) cw >>= 1;
   const int G = TF_THREADS / cw;  // lanes per column (power of two, <= 32)
   double* sU = buf;
   double* sA = buf + ib * cw;

@@ -1,0 +1,103 @@
+// kbench.cu — per-kernel throughput microbenchmark for the tile kernels of libtilefact.
+// Every CTA runs work items of one kind back to back on its own private tiles (no
+// scheduler, no dependencies), so the measured rate is the kernel's steady-state
+// per-SM throughput, directly comparable with the trace's per-item numbers.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -o build/kbench tools/kbench.cu
+//   ./build/kbench <kind> <b> <ib> [ctas_per_sm=1] [reps=4]
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+#include "../paper_0709_1272_b200/csrc/tf_kernels.cuh"
+
+using namespace tf;
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
+
+__global__ void __launch_bounds__(TF_THREADS, 1)
+kb_kernel(int kind, int b, int ib, double* tiles, double* aux, int* ipiv, double* scratch, size_t scr, int reps) {
+  extern __shared__ __align__(16) double sm[];
+  Ctx cx;
+  cx.b = b; cx.ib = ib; cx.scratch = scratch + (size_t)blockIdx.x * scr; cx.info = nullptr; cx.abort_flag = nullptr;
+  const size_t bb = (size_t)b * b;
+  double* t0 = tiles + (size_t)blockIdx.x * 3 * bb;
+  double* t1 = t0 + bb;
+  double* t2 = t1 + bb;
+  double* ax = aux + (size_t)blockIdx.x * ib * b;
+  int* pv = ipiv + (size_t)blockIdx.x * b;
+  const int nit = items_of(kind, b);
+  for (int r = 0; r < reps; ++r) {
+    const int it = (blockIdx.x + r) % nit;
+    switch (kind) {
+      case 0: potrf_item(cx, t0, sm); break;
+      case 1: trsm_item(cx, t0, t1, it, sm); break;
+      case 2: syrk_item(cx, t0, t1, it, sm); break;
+      case 3: gemm_item(cx, t0, t1, t2, it, sm); break;
+      case 4: geqrt_item(cx, t0, ax, t2, sm); break;
+      case 5: larfb_item(cx, t0, ax, t1, it, sm); break;
+      case 6: tsqrt_item(cx, t0, t1, ax, sm); break;
+      case 7: ssrfb_item(cx, t0, ax, t1, t2, it, sm); break;
+      case 8: getrf_item(cx, t0, pv, t2, sm); break;
+      case 9: gessm_item(cx, t0, pv, t1, it, sm); break;
+      case 10: tstrf_item(cx, t0, t1, ax, pv, sm); break;
+      case 11: ssssm_item(cx, t0, ax, pv, t1, t2, it, sm); break;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void init_kernel(double* x, size_t n, int b, int kind) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    // diagonally dominant, well-scaled values so repeated in-place application stays finite
+    const size_t w = e % ((size_t)b * b);
+    const int r = (int)(w % b), c = (int)(w / b);
+    double v = 1e-3 * (double)((e * 2654435761ull) % 1000) / 1000.0;
+    if (r == c) v += (kind == 0) ? 1e6 : 4.0;
+    x[e] = v;
+  }
+}
+
+int main(int argc, char** argv) {
+  const char* names[] = {"potrf", "trsm", "syrk", "gemm", "geqrt", "larfb", "tsqrt", "ssrfb", "getrf", "gessm", "tstrf", "ssssm"};
+  if (argc < 4) { fprintf(stderr, "usage: kbench kind b ib [ctas reps]\n"); return 1; }
+  int kind = -1;
+  for (int i = 0; i < 12; ++i) if (!strcmp(argv[1], names[i])) kind = i;
+  const int b = atoi(argv[2]), ib = atoi(argv[3]);
+  const int cps = argc > 4 ? atoi(argv[4]) : 1;
+  const int reps = argc > 5 ? atoi(argv[5]) : 4;
+  int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int grid = kind == 0 || kind == 4 || kind == 6 || kind == 8 || kind == 10 ? sms * cps : sms * cps;
+  const size_t bb = (size_t)b * b;
+  double *tiles, *aux, *scratch; int* ipiv;
+  const size_t scr = ((size_t)2 * ib * b + 64 + 31) & ~(size_t)31;
+  CK(cudaMalloc(&tiles, grid * 3 * bb * sizeof(double)));
+  CK(cudaMalloc(&aux, grid * (size_t)ib * b * sizeof(double)));
+  CK(cudaMalloc(&scratch, grid * scr * sizeof(double)));
+  CK(cudaMalloc(&ipiv, grid * (size_t)b * sizeof(int)));
+  CK(cudaMemset(aux, 0, grid * (size_t)ib * b * sizeof(double)));
+  // identity-ish pivots (no swaps) for gessm / ssssm
+  std::vector<int> hp(grid * (size_t)b);
+  for (size_t x = 0; x < hp.size(); ++x) hp[x] = (int)(x % b) + 1;
+  CK(cudaMemcpy(ipiv, hp.data(), hp.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaFuncSetAttribute(kb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_DOUBLES * 8));
+  init_kernel<<<1024, 256>>>(tiles, grid * 3 * bb, b, kind);
+  CK(cudaDeviceSynchronize());
+  kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, 1);
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps);
+  cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  const double fl_task[] = {b * (double)b * b / 3, (double)b * b * b, (double)b * b * (b + 1.0), 2.0 * b * b * b,
+                            4.0 * b * b * b / 3, 2.0 * b * b * b + 3.0 * ib * b * b, 2.0 * b * b * b + (double)ib * b * b,
+                            4.0 * b * b * b + (double)ib * b * b, 2.0 * b * b * b / 3, (double)b * b * b,
+                            (double)b * b * b + ib * (double)b * b / 2, 2.0 * b * b * b + (double)ib * b * b};
+  const double fl = fl_task[kind] / items_of(kind, b) * (double)grid * reps;
+  const double us_item = ms * 1e3 / reps;
+  printf("{\"kind\": \"%s\", \"b\": %d, \"ib\": %d, \"grid\": %d, \"reps\": %d, \"ms\": %.3f, \"us_per_item\": %.2f, "
+         "\"gflops_per_sm\": %.2f, \"tflops\": %.3f}\n",
+         names[kind], b, ib, grid, reps, ms, us_item, fl / (ms * 1e-3) / 1e9 / (grid / cps) , fl / (ms * 1e-3) / 1e12);
+  return 0;
+}

@@ -44,23 +44,34 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libtilefact.so (or `out`, with extra -D `defines`, for A/B experiments)."""
+    lib = out or LIB
+    if not force and out is None and not defines and not needs_build():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = ["nvcc", *NVCC_FLAGS, "-shared", "-o", tmp, *sources(), "-I", os.path.join(ROOT, "include"), "-ldl"]
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", tmp, *sources(),
+           "-I", os.path.join(ROOT, "include"), "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc build of libtilefact.so failed")
     if verbose:
         sys.stderr.write(r.stderr)
-    with open(os.path.join(HERE, "build_ptxas.log"), "w") as f:
-        f.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    if out is None:
+        with open(os.path.join(HERE, "build_ptxas.log"), "w") as f:
+            f.write(r.stderr)
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    args = sys.argv[1:]
+    out = None
+    defs = []
+    for a in args:
+        if a.startswith("--out="):
+            out = a.split("=", 1)[1]
+        elif a.startswith("-D"):
+            defs.append(a[2:])
+    print(build(force="--force" in args, verbose="-v" in args, out=out, defines=defs))

@@ -23,8 +23,68 @@
 
 namespace tf {
 
-constexpr int KC = 16;  // k-depth of one pipeline slice
-constexpr int NST = 4;  // pipeline stages
+#ifdef TF_PROBE
+// Phase timing probes (tools/kbench -DTF_PROBE): thread 0 accumulates globaltimer deltas.
+__device__ unsigned long long* g_probe;
+__device__ __forceinline__ unsigned long long probe_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TF_PROBE_MARK(slot, t0)                                                   \
+  do {                                                                           \
+    if (threadIdx.x == 0 && g_probe) {                                           \
+      unsigned long long _t = probe_now();                                       \
+      atomicAdd(&g_probe[(slot)], _t - (t0));                                    \
+      t0 = _t;                                                                   \
+    }                                                                            \
+  } while (0)
+#else
+#define TF_PROBE_MARK(slot, t0) do { } while (0)
+#endif
+
+#ifndef TF_KC
+#define TF_KC 32
+#endif
+#ifndef TF_NST
+#define TF_NST 3
+#endif
+constexpr int KC = TF_KC;   // k-depth of one pipeline slice
+constexpr int NST = TF_NST; // pipeline stages (cp.async path)
+#ifndef TF_NSTB
+#define TF_NSTB 6
+#endif
+constexpr int NSTB = TF_NSTB;  // pipeline stages of the bulk path (128x128 tiles: 6 x 33 KB)
+
+// Dynamic shared memory per CTA and the slot reserved for the bulk pipeline's mbarriers:
+// full[NSTB], empty[NSTB] and a 64-bit slice counter live in the last 16 doubles for the
+// whole kernel (initialised once by pipe_init, never re-initialised).
+constexpr int SMEM_DOUBLES = 25600;            // 200 KB
+constexpr int PIPE_OFF = SMEM_DOUBLES - 24;    // doubles (bulk + cp.async barriers, 2 counters)
+constexpr int SMEM_USER = PIPE_OFF;            // everything else fits below this
+
+__device__ __forceinline__ uint64_t* pipe_bars(double* sm) { return reinterpret_cast<uint64_t*>(sm + PIPE_OFF); }
+__device__ __forceinline__ uint64_t* pipe_bars_c(double* sm) { return pipe_bars(sm) + 2 * NSTB + 1; }
+
+// Kernel prologue: all threads call once before any Gemm::run.
+__device__ __forceinline__ void pipe_init(double* sm) {
+  uint64_t* bars = pipe_bars(sm);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTB; ++s) {
+      mbar_init(&bars[s], 1);
+      mbar_init(&bars[NSTB + s], TF_WARPS);
+    }
+    bars[2 * NSTB] = 0;  // slices issued so far by this CTA (bulk path)
+    uint64_t* cb = bars + 2 * NSTB + 1;  // cp.async path: full[NST] (all threads), empty[NST] (warps)
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&cb[s], TF_THREADS);
+      mbar_init(&cb[NST + s], TF_WARPS);
+    }
+    cb[2 * NST] = 0;  // slices issued so far by this CTA (cp.async path)
+    fence_mbar_init();
+  }
+  __syncthreads();
+}
 
 template <int BM, int BN, bool AK, bool BK>
 struct GemmLayout {
@@ -47,6 +107,7 @@ struct Gemm {
   using Lay = GemmLayout<BM, BN, AK, BK>;
   static constexpr bool KPERM = Lay::KPERM;
   static constexpr int SMEM_DOUBLES = Lay::TOTAL;
+  static constexpr int BM_ = BM, BN_ = BN;
 
   double acc[MI][NI][2];
 
@@ -168,10 +229,23 @@ struct Gemm {
             b[h][2 * j2 + 1] = v.y;
           }
         }
+#ifdef TF_M16
+        if (!AK) {
+          // fragment pair (2i', 2i'+1) = rows 16i' + 2r + {0,1} = one m16n8k4 (its rows r / r+8)
 #pragma unroll
-        for (int i = 0; i < MI; ++i)
+          for (int i2 = 0; i2 < MI / 2; ++i2)
 #pragma unroll
-          for (int j = 0; j < NI; ++j) dmma(acc[i][j], a[h][i], b[h][j]);
+            for (int j = 0; j < NI; ++j)
+              dmma16(acc[2 * i2][j][0], acc[2 * i2][j][1], acc[2 * i2 + 1][j][0], acc[2 * i2 + 1][j][1],
+                     a[h][2 * i2], a[h][2 * i2 + 1], b[h][j]);
+        } else
+#endif
+        {
+#pragma unroll
+          for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NI; ++j) dmma(acc[i][j], a[h][i], b[h][j]);
+        }
       }
     }
   }
@@ -199,12 +273,116 @@ struct Gemm {
     __syncthreads();
   }
 
+  // cp.async ring synchronised by mbarriers instead of a CTA barrier per slice: every
+  // thread issues its copies of a slice and arrives on the stage's "full" barrier when they
+  // land (cp.async.mbarrier.arrive.noinc); each warp waits on "full", computes, and arrives
+  // on "empty".  The refill of the stage consumed one slice earlier is issued after the
+  // current slice's math, when its "empty" phase has (almost always) completed, so warps
+  // drift freely inside the ring.  Stage/phase state persists across calls (slice counter).
+  template <int VEC>
+  __device__ __forceinline__ void run_mb(double* sm, const double* A, int lda, const double* B, int ldb, int M,
+                                         int N, int K) {
+    uint64_t* full = pipe_bars_c(sm);
+    uint64_t* empty = full + NST;
+    uint64_t* counter = full + 2 * NST;
+    const int nk = (K + KC - 1) / KC;
+    const uint32_t base = (uint32_t)*reinterpret_cast<volatile uint64_t*>(counter);
+    __syncthreads();  // earlier shared-memory users of the stage buffers are done
+    auto fill = [&](int kt) {
+      const uint32_t g = base + kt;
+      const int s = g % NST;
+      const uint32_t use = g / NST;
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      load_slice<VEC>(sm, s, A, lda, B, ldb, M, N, K, kt);
+      cp_async_mbar_arrive(&full[s]);
+    };
+    for (int kt = 0; kt < NST - 1 && kt < nk; ++kt) fill(kt);
+    const int lane = threadIdx.x & 31;
+    for (int kt = 0; kt < nk; ++kt) {
+      const uint32_t g = base + kt;
+      const int s = g % NST;
+      mbar_wait(&full[s], (g / NST) & 1);
+      compute_slice(sm, s);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (kt + NST - 1 < nk) fill(kt + NST - 1);
+    }
+    __syncthreads();
+    *reinterpret_cast<volatile uint64_t*>(counter) = base + nk;
+  }
+
+  // Full-tile fast path for m/n-contiguous operands: one elected producer thread streams
+  // each k-slice with bulk async copies (one per operand column, BM*8 / BN*8 bytes) into the
+  // padded stage buffers and signals a per-stage "full" mbarrier by transaction bytes;
+  // every warp waits on "full", computes, and arrives on the stage's "empty" mbarrier,
+  // which the producer waits on before refilling.  No CTA-wide barrier per slice.
+  __device__ __forceinline__ void run_bulk(double* sm, const double* A, int lda, const double* B, int ldb,
+                                           int K) {
+    uint64_t* full = pipe_bars(sm);
+    uint64_t* empty = full + NSTB;
+    uint64_t* counter = full + 2 * NSTB;
+    const int nk = K / KC;
+    const uint32_t base = (uint32_t)*reinterpret_cast<volatile uint64_t*>(counter);
+    // Callers that stored an operand themselves issue fence_proxy_async_all() from every
+    // writing thread before calling; here: all earlier shared-memory use of the stage
+    // buffers is finished, and the producer orders its own view before the bulk copies.
+    __syncthreads();
+    if (threadIdx.x == 0) fence_proxy_async_all();
+    constexpr uint32_t BYTES = (uint32_t)(KC * (BM + BN) * 8);
+    // slice kt of this call is the CTA's (base + kt)-th slice: stage g % NST, use g / NST
+    auto produce = [&](int kt) {
+      const uint32_t g = base + kt;
+      const int s = g % NSTB;
+      const uint32_t use = g / NSTB;
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);  // previous contents consumed
+      double* sA = sm + s * Lay::STAGE;
+      double* sB = sA + Lay::A_ELEMS;
+      mbar_arrive_tx(&full[s], BYTES);
+      const double* a = A + (size_t)kt * KC * lda;
+      const double* b = B + (size_t)kt * KC * ldb;
+#pragma unroll 4
+      for (int k = 0; k < KC; ++k) {
+        bulk_g2s(sA + k * Lay::SMN_A, a + (size_t)k * lda, BM * 8, &full[s]);
+        bulk_g2s(sB + k * Lay::SMN_B, b + (size_t)k * ldb, BN * 8, &full[s]);
+      }
+    };
+    if (threadIdx.x == 0)
+      for (int kt = 0; kt < NSTB && kt < nk; ++kt) produce(kt);
+    const int lane = threadIdx.x & 31;
+    for (int kt = 0; kt < nk; ++kt) {
+      const uint32_t g = base + kt;
+      const int s = g % NSTB;
+      mbar_wait(&full[s], (g / NSTB) & 1);
+      compute_slice(sm, s);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (threadIdx.x == 0 && kt + NSTB < nk) produce(kt + NSTB);
+    }
+    __syncthreads();
+    // every thread stores the same value, so each thread's next read sees base + nk
+    *reinterpret_cast<volatile uint64_t*>(counter) = base + nk;
+  }
+
   __device__ __forceinline__ void run(double* sm, const double* A, int lda, const double* B, int ldb, int M,
                                       int N, int K) {
     const bool v2 = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
                     ((lda | ldb) & 1) == 0;
+    // bulk pipeline only where a slice's math (BM*BN*KC/8/16 DMMAs per warp) hides the
+    // producer's 2*KC copy issues: the full 128x128 tiles of GEMM / SYRK
+#ifdef TF_BULK
+    if (!AK && !BK && BM >= 128 && BN >= 128 && NSTB * Lay::STAGE <= SMEM_USER && v2 && M == BM && N == BN &&
+        K % KC == 0 && K >= KC) {
+      run_bulk(sm, A, lda, B, ldb, K);
+      return;
+    }
+#endif
+#ifdef TF_SYNC_RING
     if (v2) run_v<2>(sm, A, lda, B, ldb, M, N, K);
     else run_v<1>(sm, A, lda, B, ldb, M, N, K);
+#else
+    if (v2) run_mb<2>(sm, A, lda, B, ldb, M, N, K);
+    else run_mb<1>(sm, A, lda, B, ldb, M, N, K);
+#endif
   }
 
   // f(r, c, v) for every accumulator element inside [0,M) x [0,N) (undoing the labels).

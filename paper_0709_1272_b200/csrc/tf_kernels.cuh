@@ -23,7 +23,6 @@
 
 namespace tf {
 
-constexpr int SMEM_DOUBLES = 25600;  // 200 KB dynamic shared memory per CTA
 constexpr int RB = 128;              // TRSM row block / SYRK-GEMM sub-tile edge
 constexpr int NS = 64;               // column-slab width of LARFB/SSRFB/GESSM/SSSSM items
 constexpr int NB = 32;               // column block of the in-CTA POTRF / TRSM solves
@@ -202,6 +201,7 @@ __device__ inline int potrf_item(const Ctx& cx, double* A, double* sm) {
       if (r >= c) A[jb + r + (size_t)(jb + c) * b] = D[r + c * (NB + 1)];
     }
     row_solve(A + jb + nb + (size_t)jb * b, b, b - jb - nb, nb, D);
+    fence_proxy_async_all();  // the next column block's bulk copies read what was just stored
     __syncthreads();
   }
   return -1;
@@ -216,6 +216,9 @@ __device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int 
   X += r0;
   for (int jb = 0; jb < b; jb += NB) {
     const int nb = min(NB, b - jb);
+#ifdef TF_DEBUG_TRACE
+    if (threadIdx.x == 0) printf("trsm blk %d jb %d\n", blockIdx.x, jb);
+#endif
     if (jb > 0) {
       GemmNT32 g;
       g.zero();
@@ -224,6 +227,7 @@ __device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int 
     }
     load_lower_block(D, L + jb + (size_t)jb * b, b, nb);  // (has __syncthreads)
     row_solve(X + (size_t)jb * b, b, rows, nb, D);
+    fence_proxy_async_all();  // the next block's bulk copies read the rows just solved
     __syncthreads();
   }
 }
@@ -251,11 +255,18 @@ __device__ inline void gemm_item(const Ctx& cx, const double* A, const double* B
   const int mi = item % nr, ni = item / nr;
   const int m0 = mi * RB, n0 = ni * RB;
   const int mm = min(RB, b - m0), nn = min(RB, b - n0);
+#ifdef TF_PROBE
+  unsigned long long t0 = probe_now();
+#endif
   prefetch_l2(C + m0 + (size_t)n0 * b, b, mm, nn);
   GemmNT128 g;
   g.zero();
+  TF_PROBE_MARK(0, t0);
   g.run(sm, A + m0, b, B + n0, b, mm, nn, b);
+  TF_PROBE_MARK(1, t0);
   sub_store(g, C + m0 + (size_t)n0 * b, b, mm, nn);
+  __syncthreads();
+  TF_PROBE_MARK(2, t0);
 }
 
 // ====================================================================================
@@ -329,7 +340,7 @@ __device__ inline void geqrt_item(const Ctx& cx, double* A, double* Tst, double*
   double* W2 = W + (size_t)ib * b;
   for (int c0 = 0; c0 < b; c0 += ib) {
     const int c1 = c0 + ib, mp = b - c0;
-    const bool in_smem = (size_t)mp * ib + (size_t)ib * ib + 2 * TF_WARPS + ib <= SMEM_DOUBLES;
+    const bool in_smem = (size_t)mp * ib + (size_t)ib * ib + 2 * TF_WARPS + ib <= SMEM_USER;
     double* Ts = sm;
     double* red = Ts + ib * ib;
     double* sdot = red + TF_WARPS;
@@ -447,7 +458,7 @@ __device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* T
     double* red = Rb + ib * ib;
     double* sdot = red + TF_WARPS;
     double* P = sdot + ib + TF_WARPS;
-    const bool in_smem = (size_t)b * ib + 2 * (size_t)ib * ib + 2 * TF_WARPS + ib <= SMEM_DOUBLES;
+    const bool in_smem = (size_t)b * ib + 2 * (size_t)ib * ib + 2 * TF_WARPS + ib <= SMEM_USER;
     int ldp = b;
     for (int e = tid; e < ib * ib; e += TF_THREADS) {
       const int r = e % ib, c = e / ib;
@@ -639,7 +650,7 @@ __device__ inline int getrf_item(const Ctx& cx, double* A, int* ipiv, double* LX
       }
       __syncthreads();
       swap_solve(A + c0 + (size_t)c1 * b, b, nullptr, b, ib, b - c1, nullptr, nullptr, 0, Lb, buf,
-                 SMEM_DOUBLES - ib * ib - 64);
+                 SMEM_USER - ib * ib - 64);
       update_mn(sm, A + c1 + (size_t)c1 * b, b, A + c1 + (size_t)c0 * b, b, A + c0 + (size_t)c1 * b, b, b - c1,
                 b - c1, ib);
       __syncthreads();
@@ -669,7 +680,7 @@ __device__ inline void gessm_item(const Ctx& cx, const double* LX, const int* ip
       const int t = perm[j]; perm[j] = perm[r]; perm[r] = t;
     }
   __syncthreads();
-  const int cap = SMEM_DOUBLES - (b + 1) / 2 - 8;
+  const int cap = SMEM_USER - (b + 1) / 2 - 8;
   const int cw = max(1, min(nc, cap / b));
   for (int cs = 0; cs < nc; cs += cw) {
     const int w = min(cw, nc - cs);
@@ -690,7 +701,7 @@ __device__ inline void gessm_item(const Ctx& cx, const double* LX, const int* ip
       Lb[e] = (r > c) ? ldg_cg(LX + c0 + r + (size_t)(c0 + c) * b) : 0.0;
     }
     __syncthreads();
-    swap_solve(C + c0, b, nullptr, b, ib, nc, nullptr, nullptr, 0, Lb, sm + ib * ib, SMEM_DOUBLES - ib * ib - 64);
+    swap_solve(C + c0, b, nullptr, b, ib, nc, nullptr, nullptr, 0, Lb, sm + ib * ib, SMEM_USER - ib * ib - 64);
     if (c1 < b) update_mn(sm, C + c1, b, LX + c1 + (size_t)c0 * b, b, C + c0, b, b - c1, nc, ib);
     __syncthreads();
   }
@@ -751,7 +762,7 @@ __device__ inline int tstrf_item(const Ctx& cx, double* U, double* A, double* Ls
     double* redv = Lsb + ib * ib;
     int* redi = reinterpret_cast<int*>(redv + TF_WARPS);
     double* P = redv + 2 * TF_WARPS;
-    const bool in_smem = (size_t)b * ib + 2 * (size_t)ib * ib + 2 * TF_WARPS <= SMEM_DOUBLES;
+    const bool in_smem = (size_t)b * ib + 2 * (size_t)ib * ib + 2 * TF_WARPS <= SMEM_USER;
     for (int e = tid; e < ib * ib; e += TF_THREADS) {
       const int r = e % ib, c = e / ib;
       Ub[e] = (r <= c) ? ldg_cg(U + c0 + r + (size_t)(c0 + c) * b) : 0.0;
@@ -784,7 +795,7 @@ __device__ inline int tstrf_item(const Ctx& cx, double* U, double* A, double* Ls
       __syncthreads();
       const int nslot = build_slots(ipiv, c0, ib, b, jslot, srow, rowslot, snslot);
       double* buf = Lb + ib * ib + (2 * ib + 2 + b + 1) / 2 + 2;
-      const int cap = SMEM_DOUBLES - (int)(buf - sm);
+      const int cap = SMEM_USER - (int)(buf - sm);
       swap_solve(U + c0 + (size_t)c1 * b, b, A + (size_t)c1 * b, b, ib, b - c1, jslot, srow, nslot, Lb, buf, cap);
       update_mn(sm, A + (size_t)c1 * b, b, A + (size_t)c0 * b, b, U + c0 + (size_t)c1 * b, b, b, b - c1, ib);
       __syncthreads();
@@ -810,7 +821,7 @@ __device__ inline void ssssm_item(const Ctx& cx, const double* L, const double* 
     __syncthreads();
     const int nslot = build_slots(ipiv, c0, ib, b, jslot, srow, rowslot, snslot);
     double* buf = Lb + ib * ib + (2 * ib + 2 + b + 1) / 2 + 2;
-    const int cap = SMEM_DOUBLES - (int)(buf - sm);
+    const int cap = SMEM_USER - (int)(buf - sm);
     swap_solve(U + c0, b, A, b, ib, nc, jslot, srow, nslot, Lb, buf, cap);
     update_mn(sm, A, b, L + (size_t)c0 * b, b, U + c0, b, b, nc, ib);
     __syncthreads();

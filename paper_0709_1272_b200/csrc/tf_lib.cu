@@ -89,7 +89,8 @@ __device__ inline int sched_pop(const Sched& S) {
           int v;
           while ((v = *slot) < 0) {
           }
-          __threadfence();  // acquire: the producers' tile writes are visible (and L1 is invalidated)
+          __threadfence();         // acquire: the producers' tile writes are visible (and L1 is invalidated)
+          fence_proxy_async_all();  // ... also to this thread's bulk (async-proxy) copies
           return v;
         }
         retry = true;
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tf_persistent(Prob P, Sched S) 
   cx.scratch = P.scratch + (size_t)blockIdx.x * P.scr_stride;
   cx.info = P.info;
   cx.abort_flag = S.abort_flag;
+  pipe_init(sm);
   for (;;) {
     if (threadIdx.x == 0) s_it = sched_pop(S);
     __syncthreads();
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
   cx.scratch = scratch + (size_t)blockIdx.x * scr_stride;
   cx.info = info;
   cx.abort_flag = nullptr;
+  pipe_init(sm);
   const int sub = blockIdx.x;
   int f = -1;
   switch (kind) {

@@ -26,8 +26,10 @@ kb_kernel(int kind, int b, int ib, double* tiles, double* aux, int* ipiv, double
   double* ax = aux + (size_t)blockIdx.x * ib * b;
   int* pv = ipiv + (size_t)blockIdx.x * b;
   const int nit = items_of(kind, b);
+  pipe_init(sm);
   for (int r = 0; r < reps; ++r) {
     const int it = (blockIdx.x + r) % nit;
+    if (threadIdx.x == 0) fence_proxy_async_all();
     switch (kind) {
       case 0: potrf_item(cx, t0, sm); break;
       case 1: trsm_item(cx, t0, t1, it, sm); break;
@@ -90,6 +92,18 @@ int main(int argc, char** argv) {
   cudaEventRecord(e1);
   CK(cudaEventSynchronize(e1));
   float ms; cudaEventElapsedTime(&ms, e0, e1);
+#ifdef TF_PROBE
+  {
+    unsigned long long* pr;
+    cudaMallocManaged(&pr, 8 * sizeof(unsigned long long));
+    for (int i = 0; i < 8; ++i) pr[i] = 0;
+    cudaMemcpyToSymbol(g_probe, &pr, sizeof(pr));
+    kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps);
+    CK(cudaDeviceSynchronize());
+    printf("probe us/item: pre %.2f main %.2f epi %.2f\n", pr[0] / 1e3 / grid / reps, pr[1] / 1e3 / grid / reps,
+           pr[2] / 1e3 / grid / reps);
+  }
+#endif
   const double fl_task[] = {b * (double)b * b / 3, (double)b * b * b, (double)b * b * (b + 1.0), 2.0 * b * b * b,
                             4.0 * b * b * b / 3, 2.0 * b * b * b + 3.0 * ib * b * b, 2.0 * b * b * b + (double)ib * b * b,
                             4.0 * b * b * b + (double)ib * b * b, 2.0 * b * b * b / 3, (double)b * b * b,

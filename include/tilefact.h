@@ -51,7 +51,7 @@ typedef struct CUstream_st* tf_stream_t; /* = cudaStream_t; NULL = legacy defaul
 
 #define TF_ERR_CUDA 1     /* a CUDA runtime call failed (see tile_strerror / tile_last_error) */
 #define TF_ERR_NOMEM 2    /* device allocation for library scratch failed */
-#define TF_ERR_NCCL 3     /* NCCL call failed (multi-GPU entry points) */
+#define TF_ERR_NCCL 3     /* reserved (the multi-GPU data path does not use NCCL) */
 #define TF_ERR_UNSUPPORTED 4 /* configuration not supported by this build */
 
 /* Largest tile size accepted (the in-CTA panel kernels keep O(b) state per thread). */
@@ -126,18 +126,69 @@ int64_t tile_dag_export(int alg, int64_t p, int policy, int32_t* kind, int32_t* 
 int tk_run(int kind, int64_t b, int64_t ib, double* t0, double* t1, double* t2, double* aux,
            int32_t* ipiv, int32_t* d_info, tf_stream_t stream);
 
-/* Multi-GPU SPMD entry points (one call per rank, P x Q 2D block-cyclic owner-computes
- * tile distribution, tile (i,j) on rank (i mod P) + (j mod Q)*P ... see DESIGN.md §7).
- * dA_loc holds this rank's tiles ordered column-major by local (i,j); nccl_comm is an
- * ncclComm_t for the P*Q ranks.  Panel tiles are broadcast with NCCL. */
-int tile_chol_dist(int64_t n, int64_t b, int64_t ib, int P, int Q, double* dA_loc,
-                   int32_t* d_info, void* nccl_comm, tf_stream_t stream);
-int64_t tile_dist_local_tiles(int64_t n, int64_t b, int P, int Q, int rank, int lower_only);
-/* NCCL bootstrap helpers (the unique id travels over torch.distributed). */
-int tile_nccl_id_bytes(void);
-int tile_nccl_get_unique_id(void* id_out);
-int tile_nccl_comm_init(void* id, int nranks, int rank, void** comm_out);
-int tile_nccl_comm_destroy(void* comm);
+/* ---------------------------------------------------------------------------------
+ * Multi-GPU (PAPER.md:972-1049 for the DAG runtime it distributes).
+ * Owner computes on a P x Q 2D block-cyclic tile grid: tile (i,j) lives on rank
+ * (i mod P)*Q + (j mod Q) and every task runs on the owner of the tile it writes
+ * (QR / LU: P must be 1, a column-cyclic grid, so the flat TSQRT/TSTRF chains and the
+ * R/U row updates stay on one rank).  Each rank stores its tiles ("local BDL") ordered
+ * column-major by local tile index: tile (i,j) at ((i/P) + (j/Q)*ceil(p/P)) * b*b; its
+ * T / L strips and pivot vectors use the same local index (strip stride ib*b, pivot
+ * stride b).  Panel results cross ranks inside the persistent kernel: the producing rank
+ * stores the tile (L_kk / L_ik; V_kk + T_kk, V_ik + T_ik; L_kk + ipiv, L_ik + Ls + ipiv)
+ * directly into each consumer's receive cache over NVLink and pushes the consumer's
+ * RECV task into its ready queue with system-scope atomics; there is no host proxy.
+ * Results are bitwise identical to the 1-GPU factorization (same kernels, same per-tile
+ * update order).  b must be a multiple of 4; P*Q <= 8.
+ *
+ * Protocol (one process per GPU, all ranks collectively, in the same order):
+ *   tile_dist_open    -> this rank's IPC handle (tile_dist_ipc_bytes() bytes)
+ *   (gather all handles in rank order, e.g. torch.distributed.all_gather)
+ *   tile_dist_connect -> maps every peer's symmetric block
+ *   tile_dist_factor  -> enqueue one factorization on `stream` (repeatable)
+ *   tile_dist_close
+ * d_info (device int32, written at the end): LAPACK semantics combined over all ranks
+ * (min failing column), or -1 if a peer did not arrive / no progress was made for
+ * TF_DIST_TIMEOUT_S seconds (default 120) — a protocol timeout, never a hang.
+ * Ownership: the caller owns dA_loc / dAux_loc / dIpiv_loc / d_info; the handle owns its
+ * symmetric block (scheduler state + receive cache, ~p(p+1)/2 tiles when P*Q > 1). */
+typedef struct tf_dist_s* tf_dist_t;
+
+/* alg: 0 chol, 1 qr, 2 lu.  ipc_out: tile_dist_ipc_bytes() bytes (may be NULL when
+ * P*Q == 1).  Returns 0 or -k / TF_ERR_* as above. */
+int tile_dist_open(int alg, int64_t n, int64_t b, int64_t ib, int P, int Q, int rank, void* ipc_out,
+                   tf_dist_t* out);
+int tile_dist_ipc_bytes(void);
+/* all_ipc: P*Q handles, rank order (this rank's own entry is ignored). */
+int tile_dist_connect(tf_dist_t h, const void* all_ipc);
+/* dAux_loc: T strips (qr) / L strips (lu), NULL for chol; dIpiv_loc: lu only. */
+int tile_dist_factor(tf_dist_t h, double* dA_loc, double* dAux_loc, int32_t* dIpiv_loc, int32_t* d_info,
+                     tf_stream_t stream);
+void tile_dist_close(tf_dist_t h);
+/* Elements per rank of the local buffers (same for every rank): which 0 = A (doubles),
+ * 1 = T / L strips (doubles), 2 = ipiv (int32).  -1 on invalid arguments. */
+int64_t tile_dist_local_elems(int alg, int64_t n, int64_t b, int64_t ib, int P, int Q, int which);
+/* Owner rank of tile (i,j). */
+int tile_dist_owner(int64_t i, int64_t j, int P, int Q);
+/* Single-GPU emulation of a P x Q job (tests, and the only way to run the multi-rank
+ * path on one GPU): ONE persistent launch whose CTAs are split into P*Q groups, each
+ * running one rank's local DAG on its own local buffers (arrays of P*Q device
+ * pointers); the peers' "NVLink" stores are same-device stores.  Same device code as
+ * tile_dist_factor.  d_info receives the combined info. */
+int tile_dist_emulate(int alg, int64_t n, int64_t b, int64_t ib, int P, int Q, double* const* dA_loc,
+                      double* const* dAux_loc, int32_t* const* dIpiv_loc, int32_t* d_info,
+                      tf_stream_t stream);
+/* Host-only export of rank `rank`'s local task graph (tests; b = ib = 4 item counts).
+ * Per local task: kind (0-11 as above, 12 SEND, 13 RECV), k, i, j (of the producing
+ * task for SEND / RECV), link (SEND: offset of its entries in send_peer/send_task;
+ * RECV: the producing rank; else -1), gid (global task id in program order; the
+ * producer's for SEND / RECV).  CSR successors as in tile_dag_export.  send_peer /
+ * send_task: the consumer rank and the RECV task id on that rank.  Returns the local
+ * task count (-1 on invalid arguments). */
+int64_t tile_dist_plan_export(int alg, int64_t p, int P, int Q, int rank, int32_t* kind, int32_t* k,
+                              int32_t* i, int32_t* j, int32_t* link, int32_t* gid, int64_t cap,
+                              int64_t* succ_off, int32_t* succ, int64_t succ_cap, int32_t* send_peer,
+                              int32_t* send_task, int64_t send_cap, int64_t* nedges, int64_t* nsends);
 
 const char* tile_strerror(int code);
 const char* tile_last_error(void);

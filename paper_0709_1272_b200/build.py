@@ -44,23 +44,59 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
+def _obj_deps(src):
+    """Headers a translation unit depends on (conservative: every header for CUDA files)."""
+    hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")))
+    inc = os.path.join(ROOT, "include", "tilefact.h")
+    if src.endswith(".cpp"):
+        hdrs = [h for h in hdrs if h.endswith(".h")]
+    return [src, inc, *hdrs]
+
+
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
-    """Build libtilefact.so (or `out`, with extra -D `defines`, for A/B experiments)."""
+    """Build libtilefact.so (or `out`, with extra -D `defines`, for A/B experiments).
+
+    Each source compiles to its own object (so host-only edits do not recompile the
+    kernels); objects are rebuilt when the source or a header it depends on changes."""
     lib = out or LIB
     if not force and out is None and not defines and not needs_build():
         return LIB
+    tag = "default" if not defines else "_".join(d.replace("=", "-") for d in defines)
+    odir = os.path.join(ROOT, "build", "obj", tag)
+    os.makedirs(odir, exist_ok=True)
+    objs, logs = [], []
+    for src in sources():
+        obj = os.path.join(odir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        if not force and os.path.exists(obj) and all(os.path.getmtime(d) <= os.path.getmtime(obj)
+                                                     for d in _obj_deps(src)):
+            log = obj + ".log"
+            if os.path.exists(log):
+                logs.append(open(log).read())
+            continue
+        tmp = obj + f".tmp{os.getpid()}"
+        cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", "-o", tmp, src,
+               "-I", os.path.join(ROOT, "include")]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"nvcc compile of {os.path.basename(src)} failed")
+        with open(obj + ".log", "w") as f:
+            f.write(r.stderr)
+        logs.append(r.stderr)
+        os.replace(tmp, obj)
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-o", tmp, *sources(),
-           "-I", os.path.join(ROOT, "include"), "-ldl"]
+    cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+           "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc build of libtilefact.so failed")
+        raise RuntimeError("nvcc link of libtilefact.so failed")
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write("".join(logs))
     if out is None:
         with open(os.path.join(HERE, "build_ptxas.log"), "w") as f:
-            f.write(r.stderr)
+            f.write("".join(logs))
     os.replace(tmp, lib)
     return lib
 

@@ -1,0 +1,1059 @@
+// tf_host.cpp — host side of libtilefact.so: the task-graph builder (Algorithms 1-3 with
+// the SURVEY §8(a) a13 dependency rules), the multi-GPU distribution plan, workspace
+// caches, and the C-ABI declared in include/tilefact.h.  No device code lives here; the
+// kernels and their launch wrappers are in tf_device.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <tuple>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/tilefact.h"
+#include "tf_sched.h"
+
+using namespace tf;
+
+namespace {
+
+thread_local char g_err[512] = "";
+void set_err(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+#define TF_CUDA(x)                                                                      \
+  do {                                                                                  \
+    cudaError_t _e = (x);                                                               \
+    if (_e != cudaSuccess) {                                                            \
+      set_err("%s: %s (%s:%d)", #x, cudaGetErrorString(_e), __FILE__, __LINE__);        \
+      return TF_ERR_CUDA;                                                               \
+    }                                                                                   \
+  } while (0)
+
+#define TF_LAUNCH(x)                                                                    \
+  do {                                                                                  \
+    int _e = (x);                                                                       \
+    if (_e) {                                                                           \
+      set_err("%s: %s", #x, cudaGetErrorString((cudaError_t)_e));                       \
+      return TF_ERR_CUDA;                                                               \
+    }                                                                                   \
+  } while (0)
+
+int g_policy = 1;
+int64_t g_trace_cap = 0;
+int g_ctas = 0;
+std::recursive_mutex g_mu;
+
+// ------------------------------------------------------------------ task graph
+struct HostDag {
+  int alg = 0, p = 0, b = 0, policy = 0;
+  std::vector<TaskD> tasks;
+  std::vector<int> succ_off, succ, indeg0, item_task, roots;
+  std::vector<SendEnt> sends;
+  int nitems = 0;
+  int qbase[NLEV + 1] = {0};
+};
+
+inline uint64_t key4(int kind, int k, int i, int j) {
+  return ((uint64_t)kind << 60) | ((uint64_t)(unsigned)k << 40) | ((uint64_t)(unsigned)i << 20) | (uint64_t)(unsigned)j;
+}
+
+int level_of(int kind, int k, int j, int policy) {
+  switch (kind) {
+    case 0: case 4: case 8: case K_SEND: case K_RECV: return 0;  // panel (and panel traffic)
+    case 1: case 6: case 10: return 1;     // couple-factor (TRSM for Cholesky)
+    case 5: case 9: return 2;              // row-update
+    default:                               // couple-update (SYRK/GEMM/SSRFB/SSSSM)
+      return (policy == 1 && j == k + 1) ? 2 : 3;
+  }
+}
+
+// Tasks of Algorithms 1-3 in program order and their predecessor lists (a13 rules).
+void global_tasks(int alg, int p, int b, int policy, std::vector<TaskD>& tasks, std::vector<std::vector<int>>& preds) {
+  std::unordered_map<uint64_t, int> id;
+  id.reserve((size_t)p * p * p / 2 + 16);
+  tasks.clear();
+  auto add = [&](int kind, int k, int i, int j) {
+    TaskD d{kind, k, i, j, items_of(kind, b), 0, level_of(kind, k, j, policy), 0};
+    id[key4(kind, k, i, j)] = (int)tasks.size();
+    tasks.push_back(d);
+  };
+  if (alg == 0) {
+    for (int k = 0; k < p; ++k) {
+      add(0, k, k, k);
+      for (int i = k + 1; i < p; ++i) add(1, k, i, k);
+      for (int i = k + 1; i < p; ++i)
+        for (int j = k + 1; j <= i; ++j) add(i == j ? 2 : 3, k, i, j);
+    }
+  } else {
+    const int F = alg == 1 ? 4 : 8, R = F + 1, C = F + 2, U = F + 3;
+    for (int k = 0; k < p; ++k) {
+      add(F, k, k, k);
+      for (int j = k + 1; j < p; ++j) add(R, k, k, j);
+      for (int i = k + 1; i < p; ++i) {
+        add(C, k, i, k);
+        for (int j = k + 1; j < p; ++j) add(U, k, i, j);
+      }
+    }
+  }
+  const int nt = (int)tasks.size();
+  preds.assign(nt, {});
+  auto get = [&](int kind, int k, int i, int j) -> int {
+    auto it = id.find(key4(kind, k, i, j));
+    return it == id.end() ? -1 : it->second;
+  };
+  for (int t = 0; t < nt; ++t) {
+    const TaskD& d = tasks[t];
+    auto& pr = preds[t];
+    auto P = [&](int x) { if (x >= 0) pr.push_back(x); };
+    const int k = d.k, i = d.i, j = d.j;
+    if (alg == 0) {
+      switch (d.kind) {
+        case 0: if (k > 0) P(get(2, k - 1, k, k)); break;
+        case 1: P(get(0, k, k, k)); if (k > 0) P(get(3, k - 1, i, k)); break;
+        case 2: P(get(1, k, i, k)); if (k > 0) P(get(2, k - 1, i, i)); break;
+        case 3: P(get(1, k, i, k)); P(get(1, k, j, k)); if (k > 0) P(get(3, k - 1, i, j)); break;
+      }
+    } else {
+      const int F = alg == 1 ? 4 : 8, R = F + 1, C = F + 2, U = F + 3;
+      if (d.kind == F) {
+        if (k > 0) P(get(U, k - 1, k, k));
+      } else if (d.kind == R) {
+        P(get(F, k, k, k));
+        if (k > 0) P(get(U, k - 1, k, j));
+      } else if (d.kind == C) {
+        P(i == k + 1 ? get(F, k, k, k) : get(C, k, i - 1, k));
+        if (k > 0) P(get(U, k - 1, i, k));
+      } else {
+        P(get(C, k, i, k));
+        P(i == k + 1 ? get(R, k, k, j) : get(U, k, i - 1, j));
+        if (k > 0) P(get(U, k - 1, i, j));
+      }
+    }
+  }
+}
+
+// CSR successors, in-degrees, work items, per-level queue bases and roots.
+void finalize_dag(HostDag& G, const std::vector<std::vector<int>>& preds) {
+  const int nt = (int)G.tasks.size();
+  G.indeg0.assign(nt, 0);
+  std::vector<int> cnt(nt + 1, 0);
+  for (int t = 0; t < nt; ++t) {
+    G.indeg0[t] = (int)preds[t].size();
+    for (int x : preds[t]) cnt[x + 1]++;
+  }
+  G.succ_off.assign(nt + 1, 0);
+  for (int t = 0; t < nt; ++t) G.succ_off[t + 1] = G.succ_off[t] + cnt[t + 1];
+  G.succ.assign(G.succ_off[nt], 0);
+  std::vector<int> fill(G.succ_off.begin(), G.succ_off.end() - 1);
+  for (int t = 0; t < nt; ++t)
+    for (int x : preds[t]) G.succ[fill[x]++] = t;
+  int lev_items[NLEV] = {0};
+  G.nitems = 0;
+  for (int t = 0; t < nt; ++t) {
+    G.tasks[t].item0 = G.nitems;
+    G.nitems += G.tasks[t].nitems;
+    lev_items[G.tasks[t].level] += G.tasks[t].nitems;
+  }
+  G.item_task.resize(G.nitems);
+  for (int t = 0; t < nt; ++t)
+    for (int x = 0; x < G.tasks[t].nitems; ++x) G.item_task[G.tasks[t].item0 + x] = t;
+  G.qbase[0] = 0;
+  for (int l = 0; l < NLEV; ++l) G.qbase[l + 1] = G.qbase[l] + lev_items[l];
+  G.roots.clear();
+  for (int t = 0; t < nt; ++t)
+    if (G.indeg0[t] == 0 && G.tasks[t].kind != K_RECV) G.roots.push_back(t);
+}
+
+void build_dag(HostDag& G, int alg, int p, int b, int policy) {
+  G.alg = alg; G.p = p; G.b = b; G.policy = policy;
+  std::vector<std::vector<int>> preds;
+  global_tasks(alg, p, b, policy, G.tasks, preds);
+  finalize_dag(G, preds);
+}
+
+// ------------------------------------------------------------------ multi-GPU plan
+// Owner computes on a P x Q block-cyclic tile grid: tile (r,c) lives on
+// rank (r mod P)*Q + (c mod Q); a task runs on the owner of the tile it writes (for
+// SSRFB/SSSSM, which write (k,j) and (i,j), P = 1 keeps both on the owner of column j).
+int out_row(const TaskD& d) {
+  switch (d.kind) {
+    case 0: case 4: case 8: return d.k;
+    case 5: case 9: return d.k;
+    case 2: return d.i;
+    default: return d.i;
+  }
+}
+int out_col(const TaskD& d) {
+  switch (d.kind) {
+    case 0: case 4: case 8: return d.k;
+    case 1: case 6: case 10: return d.k;
+    case 2: return d.i;
+    default: return d.j;
+  }
+}
+inline int tile_owner(int r, int c, int P, int Q) { return (r % P) * Q + (c % Q); }
+
+struct DistPlan {
+  int alg = 0, p = 0, b = 0, ib = 0, P = 1, Q = 1, nranks = 1, policy = 0;
+  std::vector<TaskD> gtasks;                // global tasks, program order
+  std::vector<HostDag> local;               // per rank
+  std::vector<std::vector<int>> gid;        // local task -> global task (SEND/RECV: producer's)
+  int max_tasks = 0, max_items = 0;
+};
+
+void build_plan(DistPlan& D, int alg, int p, int b, int ib, int P, int Q, int policy) {
+  D.alg = alg; D.p = p; D.b = b; D.ib = ib; D.P = P; D.Q = Q; D.nranks = P * Q; D.policy = policy;
+  const int R = D.nranks;
+  std::vector<TaskD> gt;
+  std::vector<std::vector<int>> gpred;
+  global_tasks(alg, p, b, policy, gt, gpred);
+  D.gtasks = gt;
+  const int nt = (int)gt.size();
+  std::vector<int> own(nt);
+  for (int t = 0; t < nt; ++t) own[t] = tile_owner(out_row(gt[t]), out_col(gt[t]), P, Q);
+  std::vector<std::vector<int>> gsucc(nt);
+  for (int t = 0; t < nt; ++t)
+    for (int x : gpred[t]) gsucc[x].push_back(t);
+  // consumer ranks of each producer (other than its owner)
+  std::vector<std::vector<int>> peers(nt);
+  for (int u = 0; u < nt; ++u) {
+    std::set<int> s;
+    for (int v : gsucc[u])
+      if (own[v] != own[u]) s.insert(own[v]);
+    peers[u].assign(s.begin(), s.end());
+  }
+  D.local.assign(R, HostDag());
+  D.gid.assign(R, {});
+  std::vector<std::vector<int>> recv_id(R, std::vector<int>());  // [rank][producer] -> local RECV id
+  std::vector<std::vector<int>> send_id(R);
+  for (int r = 0; r < R; ++r) {
+    HostDag& L = D.local[r];
+    L.alg = alg; L.p = p; L.b = b; L.policy = policy;
+    std::vector<int> lid(nt, -1), sid(nt, -1), rid(nt, -1);
+    auto& G = D.gid[r];
+    for (int t = 0; t < nt; ++t) {
+      if (own[t] == r) {
+        lid[t] = (int)L.tasks.size();
+        L.tasks.push_back(gt[t]);
+        G.push_back(t);
+        if (!peers[t].empty()) {
+          sid[t] = (int)L.tasks.size();
+          TaskD s{K_SEND, gt[t].k, gt[t].i, 0, (int)peers[t].size() * SEND_CHUNKS, 0, 0, gt[t].kind};
+          L.tasks.push_back(s);
+          G.push_back(t);
+        }
+      } else if (std::find(peers[t].begin(), peers[t].end(), r) != peers[t].end()) {
+        rid[t] = (int)L.tasks.size();
+        TaskD v{K_RECV, gt[t].k, gt[t].i, own[t], 1, 0, 0, gt[t].kind};
+        L.tasks.push_back(v);
+        G.push_back(t);
+      }
+    }
+    std::vector<std::vector<int>> lpred(L.tasks.size());
+    for (int v = 0; v < nt; ++v) {
+      if (own[v] != r) continue;
+      for (int u : gpred[v]) {
+        if (own[u] == r) lpred[lid[v]].push_back(lid[u]);
+        else lpred[lid[v]].push_back(rid[u]);
+      }
+    }
+    for (int u = 0; u < nt; ++u)
+      if (sid[u] >= 0) lpred[sid[u]].push_back(lid[u]);
+    finalize_dag(L, lpred);
+    // RECV tasks are released by the producer's rank: count that edge in the in-degree
+    for (size_t t = 0; t < L.tasks.size(); ++t)
+      if (L.tasks[t].kind == K_RECV) L.indeg0[t] = 1;
+    recv_id[r] = rid;
+    send_id[r] = sid;
+  }
+  // remote pushes: SEND(u) on its owner -> RECV(u) on every consumer rank
+  for (int r = 0; r < R; ++r) {
+    HostDag& L = D.local[r];
+    for (size_t t = 0; t < L.tasks.size(); ++t) {
+      TaskD& d = L.tasks[t];
+      if (d.kind != K_SEND) continue;
+      const int u = D.gid[r][t];
+      d.j = (int)L.sends.size();
+      for (int q : peers[u]) {
+        const HostDag& C = D.local[q];
+        const int rt = recv_id[q][u];
+        const int lev = C.tasks[rt].level;
+        L.sends.push_back(SendEnt{q, C.tasks[rt].item0, lev, C.qbase[lev], C.qbase[lev + 1]});
+      }
+    }
+  }
+  D.max_tasks = D.max_items = 0;
+  for (auto& L : D.local) {
+    D.max_tasks = std::max(D.max_tasks, (int)L.tasks.size());
+    D.max_items = std::max(D.max_items, L.nitems);
+  }
+}
+
+struct DevDag {
+  std::shared_ptr<HostDag> h;
+  TaskD* tasks = nullptr;
+  int *succ_off = nullptr, *succ = nullptr, *item_task = nullptr, *indeg0 = nullptr, *roots = nullptr;
+  SendEnt* sends = nullptr;
+};
+
+std::map<std::tuple<int, int, int, int, int>, DevDag> g_dags;  // (dev, alg, p, b, policy)
+
+template <class T>
+int upload(T** dst, const std::vector<T>& v) {
+  TF_CUDA(cudaMalloc(dst, sizeof(T) * (v.empty() ? 1 : v.size())));
+  if (!v.empty()) TF_CUDA(cudaMemcpy(*dst, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+int upload_dag(DevDag& D) {
+  int rc;
+  if ((rc = upload(&D.tasks, D.h->tasks))) return rc;
+  if ((rc = upload(&D.succ_off, D.h->succ_off))) return rc;
+  if ((rc = upload(&D.succ, D.h->succ))) return rc;
+  if ((rc = upload(&D.item_task, D.h->item_task))) return rc;
+  if ((rc = upload(&D.indeg0, D.h->indeg0))) return rc;
+  if ((rc = upload(&D.roots, D.h->roots))) return rc;
+  if ((rc = upload(&D.sends, D.h->sends))) return rc;
+  return 0;
+}
+void free_dag(DevDag& D) {
+  cudaFree(D.tasks);
+  cudaFree(D.succ_off);
+  cudaFree(D.succ);
+  cudaFree(D.item_task);
+  cudaFree(D.indeg0);
+  cudaFree(D.roots);
+  cudaFree(D.sends);
+  D = DevDag();
+}
+
+int get_dag(int dev, int alg, int p, int b, DevDag** out) {
+  auto key = std::make_tuple(dev, alg, p, b, g_policy);
+  auto it = g_dags.find(key);
+  if (it != g_dags.end()) { *out = &it->second; return 0; }
+  DevDag D;
+  D.h = std::make_shared<HostDag>();
+  build_dag(*D.h, alg, p, b, g_policy);
+  int rc;
+  if ((rc = upload_dag(D))) return rc;
+  auto res = g_dags.emplace(key, D);
+  *out = &res.first->second;
+  return 0;
+}
+
+// ------------------------------------------------------------------ workspaces
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+int ensure(Buf& b, size_t bytes) {
+  if (b.bytes >= bytes && b.p) return 0;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    set_err("cudaMalloc(%zu) failed", bytes);
+    return TF_ERR_NOMEM;
+  }
+  b.bytes = bytes;
+  return 0;
+}
+void release(Buf& b) {
+  if (b.p) cudaFree(b.p);
+  b = Buf();
+}
+
+struct Workspace {
+  Buf state, q, vx, scratch, info, trace;
+  Buf hostA, hostAux, hostPiv;  // device buffers for tile_factor_host
+  int64_t last_items = 0;
+  cudaStream_t stream = nullptr;
+};
+std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
+
+int g_nsm[64] = {0};
+bool g_attr_set[64] = {false};
+Workspace* g_last_ws = nullptr;
+
+int device_setup(int dev) {
+  if (dev >= 64) { set_err("device id %d too large", dev); return TF_ERR_UNSUPPORTED; }
+  if (!g_attr_set[dev]) {
+    TF_CUDA(cudaDeviceGetAttribute(&g_nsm[dev], cudaDevAttrMultiProcessorCount, dev));
+    TF_LAUNCH(device_kernel_setup(smem_bytes()));
+    g_attr_set[dev] = true;
+  }
+  return 0;
+}
+
+size_t scr_stride_for(int b, int ib) { return ((size_t)2 * ib * b + 64 + 31) & ~(size_t)31; }
+
+int check_args(int64_t n, int64_t b, int64_t ib, const void* dA) {
+  if (n <= 0) { set_err("n must be > 0"); return -1; }
+  if (b <= 0 || n % b) { set_err("b must be > 0 and divide n"); return -2; }
+  if (b > TF_MAX_B) { set_err("b > TF_MAX_B"); return -2; }
+  if (ib <= 0 || b % ib) { set_err("ib must be > 0 and divide b"); return -3; }
+  if (!dA) { set_err("null matrix pointer"); return -4; }
+  if ((n / b) > (1 << 19)) { set_err("too many tiles"); return -1; }
+  return 0;
+}
+
+// State layout [indeg | items_done | head | tail | ndone abort exit]; `stride` >= the task
+// count (multi-GPU: the max over ranks, so `tail` sits at the same offset on every rank).
+void fill_sched(Sched& S, const HostDag& H, const DevDag& D, int* st, int* q, int stride = -1) {
+  const int nt = (int)H.tasks.size();
+  const int ns = stride < 0 ? nt : stride;
+  S.tasks = D.tasks;
+  S.succ_off = D.succ_off;
+  S.succ = D.succ;
+  S.item_task = D.item_task;
+  S.ntasks = nt;
+  S.nitems = H.nitems;
+  for (int l = 0; l <= NLEV; ++l) S.qbase[l] = H.qbase[l];
+  S.indeg = st;
+  S.items_done = st + ns;
+  S.head = st + 2 * ns;
+  S.tail = S.head + NLEV;
+  S.ndone = S.tail + NLEV;
+  S.abort_flag = S.ndone + 1;
+  S.exit_count = S.ndone + 2;
+  S.q = q;
+  S.trace = nullptr;
+  S.trace_cap = 0;
+}
+
+int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, double* aux, int32_t* ipiv,
+                      int32_t* d_info, cudaStream_t stream) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  int dev;
+  TF_CUDA(cudaGetDevice(&dev));
+  int rc;
+  if ((rc = device_setup(dev))) return rc;
+  const int p = (int)(n / b);
+  DevDag* D;
+  if ((rc = get_dag(dev, alg, p, (int)b, &D))) return rc;
+  const HostDag& H = *D->h;
+  Workspace& W = g_ws[std::make_pair(dev, stream)];
+  W.stream = stream;
+  const int nt = (int)H.tasks.size();
+  const int ctas = g_ctas > 0 ? g_ctas : g_nsm[dev];
+  const size_t state_ints = (size_t)2 * nt + 2 * NLEV + 8;
+  if ((rc = ensure(W.state, state_ints * sizeof(int)))) return rc;
+  if ((rc = ensure(W.q, (size_t)H.nitems * sizeof(int)))) return rc;
+  if (alg != 0 && (rc = ensure(W.vx, (size_t)p * b * b * sizeof(double)))) return rc;
+  const size_t scr = scr_stride_for((int)b, (int)ib);
+  if ((rc = ensure(W.scratch, scr * ctas * sizeof(double)))) return rc;
+  if ((rc = ensure(W.info, 64))) return rc;
+  if (g_trace_cap > 0 && (rc = ensure(W.trace, (size_t)H.nitems * 5 * sizeof(long long)))) return rc;
+  static Runs R;  // large; guarded by g_mu
+  memset(&R, 0, sizeof(R));
+  R.nruns = 1;
+  Sched& S = R.r[0].S;
+  fill_sched(S, H, *D, (int*)W.state.p, (int*)W.q.p);
+  S.trace = g_trace_cap > 0 ? (long long*)W.trace.p : nullptr;
+  S.trace_cap = g_trace_cap > 0 ? H.nitems : 0;
+  W.last_items = g_trace_cap > 0 ? H.nitems : 0;
+  Prob& P = R.r[0].P;
+  P.A = dA;
+  P.aux = aux;
+  P.ipiv = ipiv;
+  P.vx = (double*)W.vx.p;
+  P.scratch = (double*)W.scratch.p;
+  P.scr_stride = scr;
+  P.n = (int)n;
+  P.b = (int)b;
+  P.ib = (int)ib;
+  P.p = p;
+  P.info = d_info ? d_info : (int*)W.info.p;
+  TF_LAUNCH(launch_sched_reset(S, D->indeg0, H.nitems, P.info, stream));
+  TF_LAUNCH(launch_sched_seed(S, D->roots, (int)H.roots.size(), stream));
+  TF_LAUNCH(launch_persistent(R, ctas, smem_bytes(), stream));
+  g_last_ws = &W;
+  return 0;
+}
+
+// ------------------------------------------------------------------ multi-GPU ranks
+// One DistRank per (rank, process): the rank's local DAG on the device, its symmetric
+// block (sync flags, scheduler state, queue, receive cache) and the peers' mapped blocks.
+struct DistRank {
+  std::shared_ptr<DistPlan> plan;
+  int rank = 0, dev = 0;
+  int64_t n = 0;
+  DevDag dag;
+  Buf sym, vx, scratch, ptab;
+  size_t off_state = 0, off_q = 0, off_ctile = 0, off_cstrip = 0, off_cpiv = 0, sym_bytes = 0;
+  char* peer_sym[TF_MAX_RANKS] = {nullptr};
+  bool ipc_opened[TF_MAX_RANKS] = {false};
+  const void* key[3] = {nullptr, nullptr, nullptr};
+  int epoch = 0;
+  bool connected = false;
+};
+
+std::map<std::tuple<int, int, int, int, int, int, int, int>, std::shared_ptr<DistPlan>> g_plans;
+
+std::shared_ptr<DistPlan> get_plan(int alg, int p, int b, int ib, int P, int Q) {
+  auto key = std::make_tuple(alg, p, b, ib, P, Q, g_policy, 0);
+  auto it = g_plans.find(key);
+  if (it != g_plans.end()) return it->second;
+  auto pl = std::make_shared<DistPlan>();
+  build_plan(*pl, alg, p, b, ib, P, Q, g_policy);
+  g_plans[key] = pl;
+  return pl;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// local storage: rank's tiles (i,j) at (i/P + (j/Q)*pl) with pl = ceil(p/P) rows
+inline int64_t loc_rows(int p, int P) { return (p + P - 1) / P; }
+inline int64_t loc_cols(int p, int Q) { return (p + Q - 1) / Q; }
+
+int check_dist_args(int alg, int64_t n, int64_t b, int64_t ib, int P, int Q) {
+  if (alg < 0 || alg > 2) { set_err("alg must be 0 (chol), 1 (qr) or 2 (lu)"); return -1; }
+  if (n <= 0) { set_err("n must be > 0"); return -2; }
+  if (b <= 0 || n % b || b > TF_MAX_B) { set_err("b must be > 0 and divide n"); return -3; }
+  if (b % 4) { set_err("multi-GPU needs b %% 4 == 0 (16-byte payload chunks)"); return -3; }
+  if (ib <= 0 || b % ib) { set_err("ib must be > 0 and divide b"); return -4; }
+  if (P <= 0 || Q <= 0 || P * Q > TF_MAX_RANKS) { set_err("P*Q must be in [1, %d]", TF_MAX_RANKS); return -5; }
+  if (alg != 0 && P != 1) { set_err("QR/LU use a 1 x Q column-cyclic grid (P must be 1)"); return -5; }
+  return 0;
+}
+
+int dist_create(DistRank& X, int alg, int64_t n, int64_t b, int64_t ib, int P, int Q, int rank) {
+  X.plan = get_plan(alg, (int)(n / b), (int)b, (int)ib, P, Q);
+  X.rank = rank;
+  X.n = n;
+  TF_CUDA(cudaGetDevice(&X.dev));
+  int rc;
+  if ((rc = device_setup(X.dev))) return rc;
+  const DistPlan& pl = *X.plan;
+  const int p = pl.p;
+  const size_t bb = (size_t)b * b;
+  const size_t nslots = pl.nranks > 1 ? (size_t)p * (p + 1) / 2 : 0;
+  X.off_state = SY_INTS * sizeof(int);
+  const size_t state_ints = (size_t)2 * pl.max_tasks + 2 * NLEV + 8;
+  X.off_q = align256(X.off_state + state_ints * sizeof(int));
+  X.off_ctile = align256(X.off_q + (size_t)pl.max_items * sizeof(int));
+  X.off_cstrip = X.off_ctile + nslots * bb * sizeof(double);
+  X.off_cpiv = X.off_cstrip + (alg != 0 ? nslots * ib * b * sizeof(double) : 0);
+  X.sym_bytes = align256(X.off_cpiv + (alg == 2 ? nslots * b * sizeof(int) : 0));
+  if ((rc = ensure(X.sym, X.sym_bytes))) return rc;
+  TF_CUDA(cudaMemset(X.sym.p, 0, X.off_ctile));
+  TF_CUDA(cudaDeviceSynchronize());  // zeroed before the handle reaches any peer
+  if (alg != 0 && (rc = ensure(X.vx, (size_t)loc_cols(p, Q) * bb * sizeof(double)))) return rc;
+  X.dag.h = std::shared_ptr<HostDag>(X.plan, &X.plan->local[rank]);
+  if ((rc = upload_dag(X.dag))) return rc;
+  for (int r = 0; r < TF_MAX_RANKS; ++r) X.peer_sym[r] = nullptr;
+  X.peer_sym[rank] = (char*)X.sym.p;
+  return 0;
+}
+
+void dist_destroy(DistRank& X) {
+  for (int r = 0; r < TF_MAX_RANKS; ++r)
+    if (X.ipc_opened[r] && X.peer_sym[r]) cudaIpcCloseMemHandle(X.peer_sym[r]);
+  release(X.sym);
+  release(X.vx);
+  release(X.scratch);
+  release(X.ptab);
+  free_dag(X.dag);
+}
+
+// Pointer tables for this call's local buffers (rebuilt only when the buffers change).
+int dist_tables(DistRank& X, double* dA, double* dAux, int32_t* dPiv, cudaStream_t stream) {
+  if (X.key[0] == dA && X.key[1] == dAux && X.key[2] == dPiv && X.ptab.p) return 0;
+  const DistPlan& pl = *X.plan;
+  const int p = pl.p, P = pl.P, Q = pl.Q;
+  const size_t bb = (size_t)pl.b * pl.b, sb = (size_t)pl.ib * pl.b;
+  const int64_t lr = loc_rows(p, P);
+  const size_t np2 = (size_t)p * p;
+  std::vector<uintptr_t> tab(3 * np2 + p, 0);
+  char* sym = (char*)X.sym.p;
+  for (int j = 0; j < p; ++j)
+    for (int i = 0; i < p; ++i) {
+      const size_t e = i + (size_t)j * p;
+      const size_t loc = (size_t)(i / P) + (size_t)(j / Q) * lr;
+      if (tile_owner(i, j, P, Q) == X.rank) {
+        tab[e] = (uintptr_t)(dA + loc * bb);
+        if (dAux) tab[np2 + e] = (uintptr_t)(dAux + loc * sb);
+        if (dPiv) tab[2 * np2 + e] = (uintptr_t)(dPiv + loc * pl.b);
+      } else if (i >= j && pl.nranks > 1) {
+        const long long s = cache_slot(i, j, p);
+        tab[e] = (uintptr_t)(sym + X.off_ctile + s * bb * sizeof(double));
+        if (pl.alg != 0) tab[np2 + e] = (uintptr_t)(sym + X.off_cstrip + s * sb * sizeof(double));
+        if (pl.alg == 2) tab[2 * np2 + e] = (uintptr_t)(sym + X.off_cpiv + s * pl.b * sizeof(int));
+      }
+    }
+  for (int k = 0; k < p; ++k) {
+    if (pl.alg == 0) continue;
+    if (tile_owner(k, k, P, Q) == X.rank) tab[3 * np2 + k] = (uintptr_t)((double*)X.vx.p + (size_t)(k / Q) * bb);
+    else tab[3 * np2 + k] = tab[k + (size_t)k * p];  // the cache slot of (k,k) holds the V_kk / L_kk copy
+  }
+  int rc;
+  if ((rc = ensure(X.ptab, tab.size() * sizeof(uintptr_t)))) return rc;
+  TF_CUDA(cudaMemcpyAsync(X.ptab.p, tab.data(), tab.size() * sizeof(uintptr_t), cudaMemcpyHostToDevice, stream));
+  TF_CUDA(cudaStreamSynchronize(stream));  // `tab` is pageable and goes out of scope
+  X.key[0] = dA;
+  X.key[1] = dAux;
+  X.key[2] = dPiv;
+  return 0;
+}
+
+long long dist_timeout_ns() {
+  const char* e = getenv("TF_DIST_TIMEOUT_S");
+  const double s = e ? atof(e) : 120.0;
+  return s > 0 ? (long long)(s * 1e9) : 0;
+}
+
+// Fill one rank's RankRun and enqueue its reset + seed kernels.
+int dist_prepare(DistRank& X, RankRun& RR, int cta0, int nctas, double* dA, double* dAux, int32_t* dPiv,
+                 int32_t* d_info, cudaStream_t stream) {
+  const DistPlan& pl = *X.plan;
+  int rc;
+  if ((rc = dist_tables(X, dA, dAux, dPiv, stream))) return rc;
+  const size_t scr = scr_stride_for(pl.b, pl.ib);
+  if ((rc = ensure(X.scratch, scr * nctas * sizeof(double)))) return rc;
+  const HostDag& H = *X.dag.h;
+  char* sym = (char*)X.sym.p;
+  int* sync = (int*)sym;
+  Sched& S = RR.S;
+  fill_sched(S, H, X.dag, (int*)(sym + X.off_state), (int*)(sym + X.off_q), pl.max_tasks);
+  S.abort_flag = sync + SY_ABORT;
+  Prob& P = RR.P;
+  P.A = dA;
+  P.aux = dAux;
+  P.ipiv = dPiv;
+  P.vx = (double*)X.vx.p;
+  P.scratch = (double*)X.scratch.p;
+  P.scr_stride = scr;
+  P.n = (int)X.n;
+  P.b = pl.b;
+  P.ib = pl.ib;
+  P.p = pl.p;
+  P.info = sync + SY_LINFO;
+  Dist& D = RR.D;
+  const size_t np2 = (size_t)pl.p * pl.p;
+  double* const* tab = (double* const*)X.ptab.p;
+  D.nranks = pl.nranks;
+  D.rank = X.rank;
+  D.epoch = ++X.epoch;
+  D.cta0 = cta0;
+  D.nctas = nctas;
+  D.tptr = tab;
+  D.sptr = tab + np2;
+  D.pptr = (int* const*)(tab + 2 * np2);
+  D.vptr = tab + 3 * np2;
+  D.sends = X.dag.sends;
+  for (int r = 0; r < TF_MAX_RANKS; ++r) D.peer_sym[r] = X.peer_sym[r];
+  D.off_tail = X.off_state + ((size_t)2 * pl.max_tasks + NLEV) * sizeof(int);
+  D.off_q = X.off_q;
+  D.off_ctile = X.off_ctile;
+  D.off_cstrip = X.off_cstrip;
+  D.off_cpiv = X.off_cpiv;
+  D.sym_bytes = X.sym_bytes;
+  D.user_info = d_info;
+  D.timeout_ns = dist_timeout_ns();
+  TF_LAUNCH(launch_sched_reset(S, X.dag.indeg0, H.nitems, P.info, stream));
+  TF_LAUNCH(launch_sched_seed(S, X.dag.roots, (int)H.roots.size(), stream));
+  return 0;
+}
+
+struct EmuKey {
+  int dev, alg;
+  int64_t n, b, ib;
+  int P, Q, policy;
+  bool operator<(const EmuKey& o) const {
+    return std::tie(dev, alg, n, b, ib, P, Q, policy) < std::tie(o.dev, o.alg, o.n, o.b, o.ib, o.P, o.Q, o.policy);
+  }
+};
+std::map<EmuKey, std::vector<std::unique_ptr<DistRank>>> g_emu;
+std::set<DistRank*> g_handles;
+
+}  // namespace
+
+// ====================================================================================
+// C-ABI
+// ====================================================================================
+struct tf_dist_s {
+  DistRank r;
+};
+
+extern "C" {
+
+int tile_chol(int64_t n, int64_t b, int64_t ib, double* dA, int32_t* d_info, tf_stream_t stream) {
+  int rc = check_args(n, b, ib, dA);
+  if (rc) return rc;
+  return run_factorization(0, n, b, ib, dA, nullptr, nullptr, d_info, (cudaStream_t)stream);
+}
+
+int tile_qr(int64_t n, int64_t b, int64_t ib, double* dA, double* dT, tf_stream_t stream) {
+  int rc = check_args(n, b, ib, dA);
+  if (rc) return rc;
+  if (!dT) { set_err("null T pointer"); return -5; }
+  return run_factorization(1, n, b, ib, dA, dT, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+int tile_lu(int64_t n, int64_t b, int64_t ib, double* dA, double* dLs, int32_t* dIpiv, int32_t* d_info,
+            tf_stream_t stream) {
+  int rc = check_args(n, b, ib, dA);
+  if (rc) return rc;
+  if (!dLs) { set_err("null L-strip pointer"); return -5; }
+  if (!dIpiv) { set_err("null ipiv pointer"); return -6; }
+  return run_factorization(2, n, b, ib, dA, dLs, dIpiv, d_info, (cudaStream_t)stream);
+}
+
+size_t tile_qr_t_elems(int64_t n, int64_t b, int64_t ib) {
+  if (n <= 0 || b <= 0 || n % b) return 0;
+  const size_t p = n / b;
+  return p * p * (size_t)ib * b;
+}
+size_t tile_lu_l_elems(int64_t n, int64_t b, int64_t ib) { return tile_qr_t_elems(n, b, ib); }
+size_t tile_lu_ipiv_elems(int64_t n, int64_t b) {
+  if (n <= 0 || b <= 0 || n % b) return 0;
+  const size_t p = n / b;
+  return p * p * (size_t)b;
+}
+
+int tile_pack(int64_t m, int64_t n, int64_t b, const double* dDense, double* dTiles, tf_stream_t stream) {
+  if (m <= 0 || n <= 0) return -1;
+  if (b <= 0 || m % b || n % b) return -3;
+  if (!dDense) return -4;
+  if (!dTiles) return -5;
+  TF_LAUNCH(launch_pack(m, n, b, const_cast<double*>(dDense), dTiles, 0, stream));
+  return 0;
+}
+
+int tile_unpack(int64_t m, int64_t n, int64_t b, const double* dTiles, double* dDense, tf_stream_t stream) {
+  if (m <= 0 || n <= 0) return -1;
+  if (b <= 0 || m % b || n % b) return -3;
+  if (!dTiles) return -4;
+  if (!dDense) return -5;
+  TF_LAUNCH(launch_pack(m, n, b, dDense, const_cast<double*>(dTiles), 1, stream));
+  return 0;
+}
+
+int tile_factor_host(int kind, int64_t n, int64_t b, int64_t ib, double* hA, double* hAux, int32_t* hIpiv,
+                     int32_t* hInfo, tf_stream_t stream) {
+  int rc = check_args(n, b, ib, hA);
+  if (rc) return rc;
+  if (kind < 0 || kind > 2) return -1;
+  cudaStream_t s = (cudaStream_t)stream;
+  int dev;
+  TF_CUDA(cudaGetDevice(&dev));
+  Workspace* W;
+  {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    W = &g_ws[std::make_pair(dev, s)];
+  }
+  const size_t an = (size_t)n * n;
+  const size_t xn = kind == 0 ? 0 : tile_qr_t_elems(n, b, ib);
+  const size_t pn = kind == 2 ? tile_lu_ipiv_elems(n, b) : 0;
+  if ((rc = ensure(W->hostA, an * sizeof(double) + 64))) return rc;
+  if (xn && (rc = ensure(W->hostAux, xn * sizeof(double)))) return rc;
+  if (pn && (rc = ensure(W->hostPiv, pn * sizeof(int32_t) + 64))) return rc;
+  double* dA = (double*)W->hostA.p;
+  int32_t* dInfo = (int32_t*)((char*)W->hostA.p + an * sizeof(double));
+  TF_CUDA(cudaMemcpyAsync(dA, hA, an * sizeof(double), cudaMemcpyHostToDevice, s));
+  if (kind == 0) rc = tile_chol(n, b, ib, dA, dInfo, stream);
+  else if (kind == 1) rc = tile_qr(n, b, ib, dA, (double*)W->hostAux.p, stream);
+  else rc = tile_lu(n, b, ib, dA, (double*)W->hostAux.p, (int32_t*)W->hostPiv.p, dInfo, stream);
+  if (rc) return rc;
+  TF_CUDA(cudaMemcpyAsync(hA, dA, an * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (hAux && xn) TF_CUDA(cudaMemcpyAsync(hAux, W->hostAux.p, xn * sizeof(double), cudaMemcpyDeviceToHost, s));
+  if (hIpiv && pn) TF_CUDA(cudaMemcpyAsync(hIpiv, W->hostPiv.p, pn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (hInfo) {
+    if (kind == 1) *hInfo = 0;
+    else TF_CUDA(cudaMemcpyAsync(hInfo, dInfo, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  }
+  TF_CUDA(cudaStreamSynchronize(s));
+  return 0;
+}
+
+void tile_set_policy(int policy) { g_policy = (policy == 0) ? 0 : 1; }
+void tile_set_trace(int64_t cap) { g_trace_cap = cap > 0 ? cap : 0; }
+void tile_set_ctas(int ctas) { g_ctas = ctas > 0 ? ctas : 0; }
+
+int64_t tile_trace_fetch(int64_t* rec, int64_t cap) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  if (!g_last_ws || !g_last_ws->trace.p || g_last_ws->last_items == 0) return 0;
+  if (cudaStreamSynchronize(g_last_ws->stream) != cudaSuccess) return -1;
+  int64_t nrec = g_last_ws->last_items;
+  if (cap < nrec) nrec = cap;
+  if (rec && nrec > 0 &&
+      cudaMemcpy(rec, g_last_ws->trace.p, (size_t)nrec * 5 * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return -1;
+  return nrec;
+}
+
+int64_t tile_dag_export(int alg, int64_t p, int policy, int32_t* kind, int32_t* k, int32_t* i, int32_t* j,
+                        int32_t* level, int64_t cap, int64_t* succ_off, int32_t* succ, int64_t succ_cap,
+                        int64_t* nedges) {
+  if (alg < 0 || alg > 2 || p <= 0) return -1;
+  HostDag G;
+  build_dag(G, alg, (int)p, 128, policy);
+  const int64_t nt = (int64_t)G.tasks.size();
+  for (int64_t t = 0; t < nt && t < cap; ++t) {
+    if (kind) kind[t] = G.tasks[t].kind;
+    if (k) k[t] = G.tasks[t].k;
+    if (i) i[t] = G.tasks[t].i;
+    if (j) j[t] = G.tasks[t].j;
+    if (level) level[t] = G.tasks[t].level;
+  }
+  if (succ_off && cap >= nt)
+    for (int64_t t = 0; t <= nt; ++t) succ_off[t] = G.succ_off[t];
+  const int64_t ne = (int64_t)G.succ.size();
+  if (succ)
+    for (int64_t e = 0; e < ne && e < succ_cap; ++e) succ[e] = G.succ[e];
+  if (nedges) *nedges = ne;
+  return nt;
+}
+
+int tk_run(int kind, int64_t b, int64_t ib, double* t0, double* t1, double* t2, double* aux, int32_t* ipiv,
+           int32_t* d_info, tf_stream_t stream) {
+  if (kind < 0 || kind > 11) return -1;
+  if (b <= 0 || b > TF_MAX_B) return -2;
+  if (ib <= 0 || b % ib) return -3;
+  cudaStream_t s = (cudaStream_t)stream;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  int dev;
+  TF_CUDA(cudaGetDevice(&dev));
+  int rc;
+  if ((rc = device_setup(dev))) return rc;
+  Workspace& W = g_ws[std::make_pair(dev, s)];
+  const int items = items_of(kind, (int)b);
+  const size_t scr = scr_stride_for((int)b, (int)ib);
+  if ((rc = ensure(W.scratch, scr * items * sizeof(double)))) return rc;
+  if ((rc = ensure(W.vx, (size_t)b * b * sizeof(double)))) return rc;
+  double* vx = (double*)W.vx.p;
+  if (kind == 5 || kind == 9) TF_LAUNCH(launch_unit_lower(t0, vx, (int)b, s));
+  TF_LAUNCH(launch_tk(kind, (int)b, (int)ib, t0, t1, t2, aux, ipiv, vx, (double*)W.scratch.p, scr, d_info, items,
+                      smem_bytes(), s));
+  return 0;
+}
+
+// ---------------------------------------------------------------- multi-GPU
+int64_t tile_dist_local_elems(int alg, int64_t n, int64_t b, int64_t ib, int P, int Q, int which) {
+  if (check_dist_args(alg, n, b, ib, P, Q)) return -1;
+  const int p = (int)(n / b);
+  const int64_t tiles = loc_rows(p, P) * loc_cols(p, Q);
+  switch (which) {
+    case 0: return tiles * b * b;
+    case 1: return alg == 0 ? 0 : tiles * ib * b;
+    case 2: return alg == 2 ? tiles * b : 0;
+    default: return -1;
+  }
+}
+
+int tile_dist_owner(int64_t i, int64_t j, int P, int Q) {
+  if (i < 0 || j < 0 || P <= 0 || Q <= 0) return -1;
+  return tile_owner((int)i, (int)j, P, Q);
+}
+
+int64_t tile_dist_plan_export(int alg, int64_t p, int P, int Q, int rank, int32_t* kind, int32_t* k, int32_t* i,
+                              int32_t* j, int32_t* link, int32_t* gid, int64_t cap, int64_t* succ_off, int32_t* succ,
+                              int64_t succ_cap, int32_t* send_peer, int32_t* send_task, int64_t send_cap,
+                              int64_t* nedges, int64_t* nsends) {
+  if (check_dist_args(alg, p * 4, 4, 4, P, Q) || rank < 0 || rank >= P * Q) return -1;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  auto pl = get_plan(alg, (int)p, 4, 4, P, Q);
+  const HostDag& L = pl->local[rank];
+  const int64_t nt = (int64_t)L.tasks.size();
+  for (int64_t t = 0; t < nt && t < cap; ++t) {
+    const TaskD& d = L.tasks[t];
+    if (kind) kind[t] = d.kind;
+    if (k) k[t] = d.k;
+    if (i) i[t] = d.i;
+    if (j) j[t] = pl->gtasks[pl->gid[rank][t]].j;
+    if (link) link[t] = d.kind == K_SEND ? d.j : (d.kind == K_RECV ? d.j : -1);
+    if (gid) gid[t] = pl->gid[rank][t];
+  }
+  if (succ_off && cap >= nt)
+    for (int64_t t = 0; t <= nt; ++t) succ_off[t] = L.succ_off[t];
+  const int64_t ne = (int64_t)L.succ.size();
+  if (succ)
+    for (int64_t e = 0; e < ne && e < succ_cap; ++e) succ[e] = L.succ[e];
+  if (nedges) *nedges = ne;
+  const int64_t ns = (int64_t)L.sends.size();
+  for (int64_t e = 0; e < ns && e < send_cap; ++e) {
+    const SendEnt& s = L.sends[e];
+    if (send_peer) send_peer[e] = s.peer;
+    if (send_task) send_task[e] = pl->local[s.peer].item_task[s.item];
+  }
+  if (nsends) *nsends = ns;
+  return nt;
+}
+
+int tile_dist_open(int alg, int64_t n, int64_t b, int64_t ib, int P, int Q, int rank, void* ipc_out,
+                   tf_dist_t* out) {
+  int rc = check_dist_args(alg, n, b, ib, P, Q);
+  if (rc) return rc;
+  if (rank < 0 || rank >= P * Q) { set_err("rank out of range"); return -7; }
+  if (!out) return -9;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  auto* h = new tf_dist_s();
+  if ((rc = dist_create(h->r, alg, n, b, ib, P, Q, rank))) {
+    dist_destroy(h->r);
+    delete h;
+    return rc;
+  }
+  if (ipc_out) {
+    cudaIpcMemHandle_t hd;
+    if (cudaIpcGetMemHandle(&hd, h->r.sym.p) != cudaSuccess) {
+      set_err("cudaIpcGetMemHandle failed");
+      dist_destroy(h->r);
+      delete h;
+      return TF_ERR_CUDA;
+    }
+    memcpy(ipc_out, &hd, sizeof(hd));
+  }
+  g_handles.insert(&h->r);
+  *out = h;
+  return 0;
+}
+
+int tile_dist_ipc_bytes(void) { return (int)sizeof(cudaIpcMemHandle_t); }
+
+int tile_dist_connect(tf_dist_t h, const void* all_ipc) {
+  if (!h) return -1;
+  if (!all_ipc) return -2;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  DistRank& X = h->r;
+  const int R = X.plan->nranks;
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  for (int r = 0; r < R; ++r) {
+    if (r == X.rank) continue;
+    int can = 0;
+    cudaIpcMemHandle_t hd;
+    memcpy(&hd, (const char*)all_ipc + r * hb, hb);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      set_err("cudaIpcOpenMemHandle(rank %d): %s (peer access %d)", r, cudaGetErrorString(e), can);
+      return TF_ERR_CUDA;
+    }
+    X.peer_sym[r] = (char*)p;
+    X.ipc_opened[r] = true;
+  }
+  X.connected = true;
+  return 0;
+}
+
+int tile_dist_factor(tf_dist_t h, double* dA_loc, double* dAux_loc, int32_t* dIpiv_loc, int32_t* d_info,
+                     tf_stream_t stream) {
+  if (!h) return -1;
+  DistRank& X = h->r;
+  if (!dA_loc) { set_err("null local matrix"); return -2; }
+  if (X.plan->alg != 0 && !dAux_loc) { set_err("null local T/L strips"); return -3; }
+  if (X.plan->alg == 2 && !dIpiv_loc) { set_err("null local ipiv"); return -4; }
+  if (!d_info) { set_err("null d_info"); return -5; }
+  if (X.plan->nranks > 1 && !X.connected) { set_err("tile_dist_connect not called"); return TF_ERR_UNSUPPORTED; }
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  cudaStream_t s = (cudaStream_t)stream;
+  // the start/end barriers need every CTA co-resident: at most one CTA per SM
+  const int ctas = g_ctas > 0 ? std::min(g_ctas, g_nsm[X.dev]) : g_nsm[X.dev];
+  static Runs R;
+  memset(&R, 0, sizeof(R));
+  R.nruns = 1;
+  int rc;
+  if ((rc = dist_prepare(X, R.r[0], 0, ctas, dA_loc, dAux_loc, dIpiv_loc, d_info, s))) return rc;
+  TF_LAUNCH(launch_persistent(R, ctas, smem_bytes(), s));
+  return 0;
+}
+
+void tile_dist_close(tf_dist_t h) {
+  if (!h) return;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  g_handles.erase(&h->r);
+  dist_destroy(h->r);
+  delete h;
+}
+
+int tile_dist_emulate(int alg, int64_t n, int64_t b, int64_t ib, int P, int Q, double* const* dA_loc,
+                      double* const* dAux_loc, int32_t* const* dIpiv_loc, int32_t* d_info, tf_stream_t stream) {
+  int rc = check_dist_args(alg, n, b, ib, P, Q);
+  if (rc) return rc;
+  if (!dA_loc) return -7;
+  if (alg != 0 && !dAux_loc) return -8;
+  if (alg == 2 && !dIpiv_loc) return -9;
+  if (!d_info) return -10;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  int dev;
+  TF_CUDA(cudaGetDevice(&dev));
+  if ((rc = device_setup(dev))) return rc;
+  const int R = P * Q;
+  const int ctas = g_ctas > 0 ? std::min(g_ctas, g_nsm[dev]) : g_nsm[dev];  // all co-resident
+  if (ctas < R) { set_err("need at least one CTA per emulated rank"); return TF_ERR_UNSUPPORTED; }
+  EmuKey key{dev, alg, n, b, ib, P, Q, g_policy};
+  auto& ranks = g_emu[key];
+  if (ranks.empty()) {
+    for (int r = 0; r < R; ++r) {
+      ranks.emplace_back(new DistRank());
+      if ((rc = dist_create(*ranks.back(), alg, n, b, ib, P, Q, r))) {
+        for (auto& x : ranks) dist_destroy(*x);
+        ranks.clear();
+        g_emu.erase(key);
+        return rc;
+      }
+    }
+    for (int r = 0; r < R; ++r)
+      for (int q = 0; q < R; ++q) ranks[r]->peer_sym[q] = (char*)ranks[q]->sym.p;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  static Runs RUN;
+  memset(&RUN, 0, sizeof(RUN));
+  RUN.nruns = R;
+  for (int r = 0; r < R; ++r) {
+    const int c0 = (int)((int64_t)r * ctas / R), c1 = (int)((int64_t)(r + 1) * ctas / R);
+    // only rank 0 writes the caller's d_info (all ranks compute the same combined value)
+    if ((rc = dist_prepare(*ranks[r], RUN.r[r], c0, c1 - c0, dA_loc[r], dAux_loc ? dAux_loc[r] : nullptr,
+                           dIpiv_loc ? dIpiv_loc[r] : nullptr, r == 0 ? d_info : nullptr, s)))
+      return rc;
+  }
+  TF_LAUNCH(launch_persistent(RUN, ctas, smem_bytes(), s));
+  return 0;
+}
+
+// ---------------------------------------------------------------- errors, teardown
+const char* tile_strerror(int code) {
+  switch (code) {
+    case 0: return "success";
+    case TF_ERR_CUDA: return "CUDA runtime error";
+    case TF_ERR_NOMEM: return "device allocation failed";
+    case TF_ERR_NCCL: return "NCCL error";
+    case TF_ERR_UNSUPPORTED: return "unsupported configuration";
+    default: return code < 0 ? "invalid argument" : "unknown error";
+  }
+}
+
+const char* tile_last_error(void) { return g_err; }
+
+void tile_finalize(void) {
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  for (auto& kv : g_ws) {
+    Workspace& W = kv.second;
+    for (Buf* b : {&W.state, &W.q, &W.vx, &W.scratch, &W.info, &W.trace, &W.hostA, &W.hostAux, &W.hostPiv})
+      release(*b);
+  }
+  g_ws.clear();
+  for (auto& kv : g_dags) free_dag(kv.second);
+  g_dags.clear();
+  for (auto& kv : g_emu)
+    for (auto& x : kv.second) dist_destroy(*x);
+  g_emu.clear();
+  g_plans.clear();
+  g_last_ws = nullptr;
+  for (int d = 0; d < 64; ++d) g_attr_set[d] = false;
+}
+
+}  // extern "C"

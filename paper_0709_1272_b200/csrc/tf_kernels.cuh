@@ -20,11 +20,10 @@
 #pragma once
 #include <climits>
 #include "tf_gemm.cuh"
+#include "tf_sched.h"
 
 namespace tf {
 
-constexpr int RB = 128;              // TRSM row block / SYRK-GEMM sub-tile edge
-constexpr int NS = 64;               // column-slab width of LARFB/SSRFB/GESSM/SSSSM items
 constexpr int NB = 32;               // column block of the in-CTA POTRF / TRSM solves
 
 struct Ctx {
@@ -33,20 +32,6 @@ struct Ctx {
   int* info;        // INT_MAX = no failure; atomicMin of the 1-based global column
   int* abort_flag;  // set on Cholesky failure: the scheduler stops handing out work
 };
-
-__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
-
-// ------------------------------------------------------------------ item counts
-__host__ __device__ inline int items_of(int kind, int b) {
-  const int nr = ceil_div(b, RB);
-  switch (kind) {
-    case 1: return nr;                 // TRSM: row blocks
-    case 2: return nr * (nr + 1) / 2;  // SYRK: lower sub-tiles
-    case 3: return nr * nr;            // GEMM: sub-tiles
-    case 5: case 7: case 9: case 11: return ceil_div(b, NS);  // slabs
-    default: return 1;                 // panels
-  }
-}
 
 using GemmNT128 = Gemm<128, 128, 4, 4, false, false>;
 using GemmNT32 = Gemm<128, 32, 8, 2, false, false>;

@@ -1,0 +1,137 @@
+// tf_sched.h — data structures shared by the device scheduler (tf_device.cu) and the
+// host side (tf_host.cpp): task descriptors, per-factorization problem/scheduler state,
+// the multi-GPU rank context, and the launch wrappers the host calls.
+//
+// Execution model: the DAG of Algorithms 1-3 runs inside ONE
+// persistent kernel; a task is split into work items (sub-tiles / row blocks / column
+// slabs) that the CTAs pop from global-memory priority queues.  Multi-GPU:
+// each rank runs the same kernel over the tasks it owns (owner computes on a P x Q
+// block-cyclic tile grid); panel tiles cross ranks as SEND work items that store the
+// tile straight into the consumer rank's receive cache over NVLink (peer pointers) and
+// then push the consumer's RECV task into its ready queue with remote atomics.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define TF_HD __host__ __device__
+#else
+#define TF_HD
+#endif
+
+namespace tf {
+
+constexpr int NLEV = 4;              // priority levels
+constexpr int RB = 128;              // TRSM row block / SYRK-GEMM sub-tile edge
+constexpr int NS = 64;               // column-slab width of LARFB/SSRFB/GESSM/SSSSM items
+constexpr int TF_MAX_RANKS = 8;      // ranks per persistent launch (emulation) / per job
+constexpr int SEND_CHUNKS = 8;       // work items per (SEND task, peer)
+
+// task kinds: 0 POTRF 1 TRSM 2 SYRK 3 GEMM 4 GEQRT 5 LARFB 6 TSQRT 7 SSRFB
+//             8 GETRF 9 GESSM 10 TSTRF 11 SSSSM 12 SEND 13 RECV
+constexpr int K_SEND = 12, K_RECV = 13;
+
+TF_HD inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+TF_HD inline int items_of(int kind, int b) {
+  const int nr = ceil_div(b, RB);
+  switch (kind) {
+    case 1: return nr;                 // TRSM: row blocks
+    case 2: return nr * (nr + 1) / 2;  // SYRK: lower sub-tiles
+    case 3: return nr * nr;            // GEMM: sub-tiles
+    case 5: case 7: case 9: case 11: return ceil_div(b, NS);  // slabs
+    default: return 1;                 // panels, RECV
+  }
+}
+
+// SEND: j = offset into Dist::sends, pad = producer kind, nitems = npeers * SEND_CHUNKS.
+struct TaskD {
+  int kind, k, i, j;
+  int nitems, item0, level, pad;
+};
+
+struct Prob {
+  double* A;
+  double* aux;   // T strips (QR) / L strips (LU)
+  int* ipiv;
+  double* vx;    // explicit unit-lower V_kk / L_kk copies, p tiles of b*b
+  double* scratch;
+  size_t scr_stride;
+  int n, b, ib, p;
+  int* info;     // INT_MAX = no failure (rank-local accumulator in multi-GPU mode)
+};
+
+struct Sched {
+  const TaskD* tasks;
+  const int* succ_off;
+  const int* succ;
+  const int* item_task;
+  int ntasks, nitems;
+  int qbase[NLEV + 1];
+  int* indeg;
+  int* items_done;
+  int* q;
+  int* head;   // [NLEV]
+  int* tail;   // [NLEV]
+  int* ndone;
+  int* abort_flag;
+  int* exit_count;
+  long long* trace;  // 5 per item or null
+  int trace_cap;
+};
+
+// One remote push: when a SEND task completes, item `item` (the consumer's RECV task)
+// is appended to level `level` of rank `peer`'s queue (queue region starts at qbase).
+struct SendEnt {
+  int peer, item, level, qbase, qcap;  // qcap: end of that level's queue region (checks)
+};
+
+// Symmetric per-rank block ("sym"), identical offsets on every rank:
+//   [sync ints][sched state ints][queue ints][cache tiles][cache strips][cache ipiv]
+enum SyncSlot { SY_ARRIVE = 0, SY_DEPART = 8, SY_INFO = 16, SY_GO = 24, SY_ABORT = 25, SY_LINFO = 26, SY_INTS = 32 };
+
+struct Dist {
+  int nranks;        // 0 = single-GPU mode (direct BDL addressing, no barriers)
+  int rank;
+  int epoch;         // call counter, identical on every rank (barrier tag)
+  int cta0, nctas;   // this rank's CTA range in the grid
+  double* const* tptr;  // [p*p] tile (i,j) -> local storage or receive-cache slot (or null)
+  double* const* sptr;  // [p*p] T / L strip (i,k)
+  int* const* pptr;     // [p*p] ipiv vector (i,k)
+  double* const* vptr;  // [p]   explicit V_kk / L_kk copy
+  const SendEnt* sends;
+  char* peer_sym[TF_MAX_RANKS];  // every rank's sym block (peer-mapped; own included)
+  size_t off_tail, off_q, off_ctile, off_cstrip, off_cpiv;  // byte offsets inside sym
+  size_t sym_bytes;
+  int* user_info;    // caller's d_info (written once at the end)
+  long long timeout_ns;
+};
+
+struct RankRun {
+  Prob P;
+  Sched S;
+  Dist D;
+};
+
+struct Runs {
+  int nruns;
+  RankRun r[TF_MAX_RANKS];
+};
+
+// receive-cache slot of panel tile (i,k), i >= k (packed lower triangle, column k major)
+TF_HD inline long long cache_slot(int i, int k, int p) {
+  return (long long)k * p - (long long)k * (k - 1) / 2 + (i - k);
+}
+
+// launch wrappers (tf_device.cu)
+int launch_sched_reset(const Sched& S, const int* indeg0, int qtotal, int* info, void* stream);
+int launch_sched_seed(const Sched& S, const int* roots, int nroots, void* stream);
+int launch_persistent(const Runs& R, int ctas, size_t smem, void* stream);
+int launch_tk(int kind, int b, int ib, double* t0, double* t1, double* t2, double* aux, int* ipiv, double* vx,
+              double* scratch, size_t scr_stride, int* info, int items, size_t smem, void* stream);
+int launch_unit_lower(const double* A, double* X, int b, void* stream);
+int launch_pack(int64_t m, int64_t n, int64_t b, double* D, double* T, int dir, void* stream);
+int device_kernel_setup(size_t smem);
+size_t smem_bytes();
+
+}  // namespace tf

@@ -10,7 +10,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtilefact.so")
+# TILEFACT_LIB selects another build of the same library (e.g. a TF_CHECK debug build
+# from tools/); there is no fallback when it is missing.
+LIB_PATH = os.environ.get("TILEFACT_LIB") or os.path.join(_HERE, "libtilefact.so")
 
 KINDS = {"potrf": 0, "trsm": 1, "syrk": 2, "gemm": 3, "geqrt": 4, "larfb": 5, "tsqrt": 6,
          "ssrfb": 7, "getrf": 8, "gessm": 9, "tstrf": 10, "ssssm": 11}
@@ -44,12 +46,16 @@ def _load():
         "tile_set_ctas": (None, [i32]),
         "tile_dag_export": (i64, [i32, i64, i32, vp, vp, vp, vp, vp, i64, vp, vp, i64, vp]),
         "tk_run": (i32, [i32, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
-        "tile_chol_dist": (i32, [i64, i64, i64, i32, i32, vp, vp, vp, vp]),
-        "tile_dist_local_tiles": (i64, [i64, i64, i32, i32, i32, i32]),
-        "tile_nccl_id_bytes": (i32, []),
-        "tile_nccl_get_unique_id": (i32, [vp]),
-        "tile_nccl_comm_init": (i32, [vp, i32, i32, vp]),
-        "tile_nccl_comm_destroy": (i32, [vp]),
+        "tile_dist_open": (i32, [i32, i64, i64, i64, i32, i32, i32, vp, vp]),
+        "tile_dist_ipc_bytes": (i32, []),
+        "tile_dist_connect": (i32, [vp, vp]),
+        "tile_dist_factor": (i32, [vp, vp, vp, vp, vp, vp]),
+        "tile_dist_close": (None, [vp]),
+        "tile_dist_local_elems": (i64, [i32, i64, i64, i64, i32, i32, i32]),
+        "tile_dist_owner": (i32, [i64, i64, i32, i32]),
+        "tile_dist_emulate": (i32, [i32, i64, i64, i64, i32, i32, vp, vp, vp, vp, vp]),
+        "tile_dist_plan_export": (i64, [i32, i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, i64, vp, vp, i64,
+                                        vp, vp, i64, vp, vp]),
         "tile_strerror": (ctypes.c_char_p, [i32]),
         "tile_last_error": (ctypes.c_char_p, []),
         "tile_finalize": (None, []),
@@ -65,9 +71,10 @@ lib = _load()
 SYMBOLS = [
     "tile_chol", "tile_qr", "tile_lu", "tile_qr_t_elems", "tile_lu_l_elems", "tile_lu_ipiv_elems",
     "tile_pack", "tile_unpack", "tile_factor_host", "tile_set_policy", "tile_set_trace",
-    "tile_trace_fetch", "tile_set_ctas", "tile_dag_export", "tk_run", "tile_chol_dist",
-    "tile_dist_local_tiles", "tile_nccl_id_bytes", "tile_nccl_get_unique_id", "tile_nccl_comm_init",
-    "tile_nccl_comm_destroy", "tile_strerror", "tile_last_error", "tile_finalize",
+    "tile_trace_fetch", "tile_set_ctas", "tile_dag_export", "tk_run", "tile_dist_open",
+    "tile_dist_ipc_bytes", "tile_dist_connect", "tile_dist_factor", "tile_dist_close",
+    "tile_dist_local_elems", "tile_dist_owner", "tile_dist_emulate", "tile_dist_plan_export",
+    "tile_strerror", "tile_last_error", "tile_finalize",
 ]
 
 
@@ -192,6 +199,106 @@ def tk_run(kind, b, ib, t0=None, t1=None, t2=None, aux=None, ipiv=None, info=Non
 
 def tile_finalize() -> None:
     lib.tile_finalize()
+
+
+# ------------------------------------------------------------------ multi-GPU
+
+def tile_dist_local_elems(alg, n, b, ib, P, Q, which) -> int:
+    """Per-rank local buffer sizes: which 0 = A, 1 = T/L strips, 2 = ipiv."""
+    a = ALGS[alg] if isinstance(alg, str) else int(alg)
+    v = int(lib.tile_dist_local_elems(a, n, b, ib, P, Q, which))
+    if v < 0:
+        raise TileFactError(f"tile_dist_local_elems: invalid arguments: {lib.tile_last_error().decode()}")
+    return v
+
+
+def tile_dist_owner(i, j, P, Q) -> int:
+    return int(lib.tile_dist_owner(i, j, P, Q))
+
+
+def tile_dist_local_index(i, j, p, P, Q) -> int:
+    """Local tile index of global tile (i,j) on its owner (include/tilefact.h layout)."""
+    return i // P + (j // Q) * ((p + P - 1) // P)
+
+
+class DistHandle:
+    """One rank of a P x Q multi-GPU factorization (tile_dist_open / connect / factor /
+    close).  `exchange(bytes) -> list[bytes]` gathers every rank's IPC handle in rank
+    order (e.g. torch.distributed.all_gather_object)."""
+
+    def __init__(self, alg, n, b, ib, P, Q, rank, exchange=None):
+        self.alg = ALGS[alg] if isinstance(alg, str) else int(alg)
+        self.n, self.b, self.ib, self.P, self.Q, self.rank = n, b, ib, P, Q, rank
+        nb = int(lib.tile_dist_ipc_bytes())
+        buf = ctypes.create_string_buffer(nb)
+        h = ctypes.c_void_p(0)
+        _check(lib.tile_dist_open(self.alg, n, b, ib, P, Q, rank, buf, ctypes.byref(h)), "tile_dist_open")
+        self._h = h
+        if P * Q > 1:
+            if exchange is None:
+                raise TileFactError("a multi-rank DistHandle needs an `exchange` function")
+            allh = exchange(buf.raw)
+            if len(allh) != P * Q or any(len(x) != nb for x in allh):
+                raise TileFactError("IPC handle exchange returned the wrong shape")
+            blob = ctypes.create_string_buffer(b"".join(allh), nb * P * Q)
+            _check(lib.tile_dist_connect(self._h, blob), "tile_dist_connect")
+
+    def factor(self, A_loc, aux_loc=None, ipiv_loc=None, info=None, stream=None) -> None:
+        _dev_f64(A_loc, "A_loc")
+        _check(lib.tile_dist_factor(self._h, _ptr(A_loc), _ptr(aux_loc), _ptr(ipiv_loc), _ptr(info),
+                                    _stream(stream)), "tile_dist_factor")
+
+    def close(self) -> None:
+        if self._h:
+            lib.tile_dist_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def tile_dist_emulate(alg, n, b, ib, P, Q, A_locs, aux_locs=None, ipiv_locs=None, info=None, stream=None) -> None:
+    """Run a P x Q job on ONE GPU in one persistent launch (lists of per-rank tensors)."""
+    a = ALGS[alg] if isinstance(alg, str) else int(alg)
+    R = P * Q
+
+    def arr(ts):
+        if ts is None:
+            return None
+        if len(ts) != R:
+            raise TileFactError("need one local buffer per rank")
+        return (ctypes.c_void_p * R)(*[t.data_ptr() for t in ts])
+
+    _check(lib.tile_dist_emulate(a, n, b, ib, P, Q, arr(A_locs), arr(aux_locs), arr(ipiv_locs), _ptr(info),
+                                 _stream(stream)), "tile_dist_emulate")
+
+
+def tile_dist_plan_export(alg, p, P, Q, rank):
+    """Host-only: rank `rank`'s local task graph (kinds 12 SEND / 13 RECV included)."""
+    import numpy as np
+    a = ALGS[alg] if isinstance(alg, str) else int(alg)
+    ne, ns = ctypes.c_int64(0), ctypes.c_int64(0)
+    nt = lib.tile_dist_plan_export(a, p, P, Q, rank, None, None, None, None, None, None, 0, None, None, 0,
+                                   None, None, 0, ctypes.byref(ne), ctypes.byref(ns))
+    if nt < 0:
+        raise TileFactError(f"tile_dist_plan_export failed: {lib.tile_last_error().decode()}")
+    cols = {k: np.zeros(nt, dtype=np.int32) for k in ("kind", "k", "i", "j", "link", "gid")}
+    off = np.zeros(nt + 1, dtype=np.int64)
+    succ = np.zeros(max(1, ne.value), dtype=np.int32)
+    sp = np.zeros(max(1, ns.value), dtype=np.int32)
+    st = np.zeros(max(1, ns.value), dtype=np.int32)
+    P_ = lambda x: ctypes.c_void_p(x.ctypes.data)  # noqa: E731
+    lib.tile_dist_plan_export(a, p, P, Q, rank, P_(cols["kind"]), P_(cols["k"]), P_(cols["i"]), P_(cols["j"]),
+                              P_(cols["link"]), P_(cols["gid"]), nt, P_(off), P_(succ), ne.value, P_(sp), P_(st),
+                              ns.value, ctypes.byref(ne), ctypes.byref(ns))
+    cols["succ_off"] = off
+    cols["succ"] = succ[:ne.value]
+    cols["send_peer"] = sp[:ns.value]
+    cols["send_task"] = st[:ns.value]
+    return cols
 
 
 # ------------------------------------------------------------------ flop counts (PAPER.md:1116-1121)

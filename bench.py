@@ -11,6 +11,12 @@ configuration the north-star target (>= 60% of FP64 tensor peak on 1 B200) is qu
 on.  The other configs are reported in "per_factorization" (3 warm-up + 3 timed steps).
 GFLOP/s uses the paper's LAPACK counts n^3/3, 4n^3/3, 2n^3/3.
 
+With N > 1 (torchrun, one rank per GPU) the same n x n factorization is distributed over
+a P x Q block-cyclic grid (Cholesky 1x2, 2x2, 2x4; QR/LU 1xN) through tile_dist_factor:
+owner-computes, panel tiles stored straight into the consumers' receive caches over
+NVLink by the persistent kernel; `value` is the whole job's GFLOP/s (one
+factorization per step, max over ranks of the CUDA-event time), "scaling": "strong".
+
 --impl reference times the CPU oracle (oracle/, plain C, one core) on a bounded sample
 of the same workload (the reference arm of this tier; there is no reference code).
 """
@@ -264,6 +270,105 @@ def sample_size(cfg):
     return ns
 
 
+
+# ------------------------------------------------------------------ multi-GPU
+def dist_grid(kind, world):
+    """P x Q process grid: Cholesky 1x1, 1x2, 2x2, 2x4; QR/LU 1 x G."""
+    if kind == "chol":
+        return {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}.get(world, (1, world))
+    return 1, world
+
+
+def local_tiles(tf, torch, cfg, G, P, Q, rank):
+    """This rank's tiles of the global BDL matrix G, in the library's local layout."""
+    n, b, ib = cfg["n"], cfg["b"], cfg["ib"]
+    p, bb = n // b, b * b
+    src, dst = [], []
+    for j in range(p):
+        for i in range(p):
+            if tf.tile_dist_owner(i, j, P, Q) == rank:
+                src.append(i + j * p)
+                dst.append(tf.tile_dist_local_index(i, j, p, P, Q))
+    loc = torch.zeros(tf.tile_dist_local_elems(cfg["kind"], n, b, ib, P, Q, 0), dtype=torch.float64,
+                      device=G.device)
+    si = torch.tensor(src, device=G.device)
+    di = torch.tensor(dst, device=G.device)
+    for c in range(0, len(src), 256):
+        loc.view(-1, bb)[di[c:c + 256]] = G.view(-1, bb)[si[c:c + 256]]
+    return loc
+
+
+def run_dist_device(tf, torch, cfg, steps, warmup, rank, world, seed=0):
+    """One P x Q factorization per step across `world` GPUs through tile_dist_factor
+    (device-initiated panel exchange over NVLink).  Returns per-rank ms list and info."""
+    import torch.distributed as dist
+    dev = torch.device("cuda")
+    n, b, ib = cfg["n"], cfg["b"], cfg["ib"]
+    P, Q = dist_grid(cfg["kind"], world)
+    dense = make_dense(cfg, seed, dev)
+    G = torch.empty(n * n, dtype=torch.float64, device=dev)
+    tf.tile_pack(n, n, b, dense.view(-1), G)
+    del dense
+    pristine = local_tiles(tf, torch, cfg, G, P, Q, rank)
+    del G
+    torch.cuda.empty_cache()
+    work = torch.empty_like(pristine)
+    aux = piv = None
+    if cfg["kind"] != "chol":
+        aux = torch.zeros(tf.tile_dist_local_elems(cfg["kind"], n, b, ib, P, Q, 1), dtype=torch.float64, device=dev)
+    if cfg["kind"] == "lu":
+        piv = torch.zeros(tf.tile_dist_local_elems(cfg["kind"], n, b, ib, P, Q, 2), dtype=torch.int32, device=dev)
+    info = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def exchange(h):
+        out = [None] * world
+        dist.all_gather_object(out, h)
+        return out
+
+    H = tf.DistHandle(cfg["kind"], n, b, ib, P, Q, rank, exchange=exchange)
+    stream = torch.cuda.current_stream()
+    ms = []
+    for s in range(warmup + steps):
+        work.copy_(pristine)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        H.factor(work, aux, piv, info)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        if s >= warmup:
+            ms.append(e0.elapsed_time(e1))
+        if int(info.item()) != 0:
+            raise RuntimeError(f"rank {rank}: tile_dist_factor info={int(info.item())}")
+    res = {"ms": ms, "info": int(info.item()), "grid": f"{P}x{Q}"}
+    # e2e: host (pinned) local tiles -> device -> factor -> host, copies inside the region
+    res["e2e"] = None
+    if steps > 0:
+        hA = pristine.cpu().pin_memory()
+        hOut = torch.empty_like(hA).pin_memory()
+        em = []
+        for s in range(2):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            work.copy_(hA, non_blocking=True)
+            H.factor(work, aux, piv, info)
+            hOut.copy_(work, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+            em.append(e0.elapsed_time(e1))
+        res["e2e"] = {"ms": sum(em) / len(em), "h2d": hA.numel() * 8, "d2h": hOut.numel() * 8}
+        del hA, hOut
+    H.close()
+    del work, pristine, aux, piv
+    torch.cuda.empty_cache()
+    return res
+
+
 # ------------------------------------------------------------------ arms
 def run_reference(args, rank, world):
     if rank != 0:
@@ -297,25 +402,45 @@ def run_reference(args, rank, world):
     return 0
 
 
+def ncu_traffic(config):
+    """DRAM bytes (read + write) per launch of tf_persistent from the committed ncu --set
+    full capture of this config (profiles/ncu_traffic.json), or None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        e = d.get(f"config{config}")
+        return (float(e["dram_bytes_per_launch"]), e["source"]) if e else (None, None)
+    except Exception:
+        return None, None
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     from paper_0709_1272_b200 import build as tfbuild
-    tfbuild.build()
+    if rank == 0:
+        tfbuild.build()
+    if world > 1:
+        torch.distributed.barrier()
     from paper_0709_1272_b200 import tilefact as tf
     torch.cuda.set_device(local_rank)
     cfg = CONFIGS[args.config]
     n, b, ib = cfg["n"], cfg["b"], cfg["ib"]
     peak_sus, peak_burst, peak_src = fp64_peak()
-    launches_per_step = 3  # reset, seed, persistent scheduler kernel
+    launches_per_step = 3  # reset, seed, persistent scheduler kernel (per rank)
 
     # ---- headline config, device-resident
     clk = ClockSampler(local_rank)
-    want = sample_size(cfg) if (rank == 0 and not args.no_cpu) else 0
+    want = sample_size(cfg) if (rank == 0 and world == 1 and not args.no_cpu) else 0
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     clk.start()
-    res, sample = run_device(tf, torch, cfg, args.steps, args.warmup, want_sample=want)
+    sample = None
+    if world == 1:
+        res, sample = run_device(tf, torch, cfg, args.steps, args.warmup, want_sample=want)
+        grid = "1x1"
+    else:
+        res = run_dist_device(tf, torch, cfg, args.steps, args.warmup, rank, world)
+        grid = res["grid"]
     clocks = clk.stop()
     if world > 1:
         torch.distributed.barrier()
@@ -324,12 +449,13 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_step = float(t.item())
-    gflops = world * lapack_flops(cfg["kind"], n) / (ms_step * 1e-3) / 1e9
+    # whole-job throughput: ONE n x n factorization per step, shared by all ranks
+    gflops = lapack_flops(cfg["kind"], n) / (ms_step * 1e-3) / 1e9
     tflops_true = true_flops(cfg["kind"], n, b, ib) / (ms_step * 1e-3) / 1e12
 
-    # ---- other factorizations (per-factorization table)
+    # ---- other factorizations (per-factorization table, 1 GPU only)
     per = []
-    if not args.only and rank == 0:
+    if not args.only and rank == 0 and world == 1:
         for c in sorted(CONFIGS):
             if c == args.config:
                 continue
@@ -341,16 +467,24 @@ def run_ours(args, rank, world, local_rank):
                         "pct_of_fp64_peak": round(100 * g / 1e3 / peak_sus, 2), "info": r["info"],
                         "l2_flushed": r["flush"]})
 
-    # ---- end to end through the host-buffer C-ABI path
+    # ---- end to end: host buffers, copies inside the timed region
     e2e = None
-    if rank == 0 and not args.no_e2e:
+    if world == 1 and rank == 0 and not args.no_e2e:
         ems, h2d, d2h, einfo = run_e2e(tf, torch, cfg, max(1, min(args.steps, 2)))
         em = sum(ems) / len(ems)
         e2e = {"value": round(lapack_flops(cfg["kind"], n) / (em * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
                "ms_per_step": round(em, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "api": "tile_factor_host (pinned host BDL buffer)"}
+    elif world > 1 and res.get("e2e"):
+        t = torch.tensor([res["e2e"]["ms"]], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        em = float(t.item())
+        e2e = {"value": round(lapack_flops(cfg["kind"], n) / (em * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+               "ms_per_step": round(em, 3), "h2d_bytes_per_step": res["e2e"]["h2d"] * world,
+               "d2h_bytes_per_step": res["e2e"]["d2h"] * world,
+               "api": "DistHandle.factor (tile_dist_factor) on each rank's pinned host local tiles"}
 
-    # ---- CPU oracle baseline (bounded sample of the same matrix)
+    # ---- CPU oracle baseline (bounded sample of the same matrix; rank 0 at N=1 only)
     cpu = None
     if rank == 0 and sample is not None:
         g, dt = cpu_oracle_sample(cfg, sample)
@@ -359,25 +493,29 @@ def run_ours(args, rank, world, local_rank):
                          f"principal block of the same A, b={b}; {dt:.1f} s"}
 
     if rank == 0:
+        traffic, tsrc = ncu_traffic(args.config) if world == 1 else (None, None)
         line = {
             "metric": METRIC, "value": round(gflops, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded; BASELINE recipe generated on device)",
-            "config": {"workload": cfg["desc"], "n": n, "b": b, "ib": ib, "grid": "1x1" if world == 1 else f"1x{world}",
-                       "parallelism": f"dp{world}" if world > 1 else "1 GPU", "l2": "inputs (8 GiB) > L2; no flush"
-                       if not res["flush"] else "L2 flushed (256 MiB write) before each step",
+            "config": {"workload": cfg["desc"], "n": n, "b": b, "ib": ib, "grid": grid,
+                       "parallelism": "1 GPU" if world == 1 else
+                       f"{grid} block-cyclic owner-computes, panel tiles over NVLink peer stores",
+                       "l2": "inputs (8 GiB) > L2; no flush" if not res.get("flush") else
+                       "L2 flushed (256 MiB write) before each step",
                        "policy": "lookahead", "flop_count": "LAPACK n^3/3 (PAPER.md:1116-1121)"},
             "pct_of_fp64_peak": round(100 * gflops / 1e3 / (peak_sus * world), 2),
             "true_tflops": round(tflops_true, 3),
             "roofline": {"bound": "tensor", "kernel": "tf_persistent (one launch = the whole DAG)",
-                         "achieved": round(tflops_true, 3), "peak": peak_sus, "unit": "TFLOP/s",
-                         "frac": round(tflops_true / peak_sus, 4), "traffic": None,
+                         "achieved": round(tflops_true / world, 3), "peak": peak_sus, "unit": "TFLOP/s",
+                         "frac": round(tflops_true / world / peak_sus, 4),
+                         "traffic": traffic, "traffic_source": tsrc,
                          "peak_source": peak_src + "; sustained DMMA figure (kernel runs >0.1 s)",
-                         "peak_burst": peak_burst},
+                         "peak_burst": peak_burst, "per": "GPU" if world > 1 else "launch"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches_per_step * args.steps * world,
             "clocks": clocks,
             "info": res["info"],
             "resid_probe": res.get("resid_probe"),
@@ -406,7 +544,7 @@ def main():
     if world > 1:
         import torch
         torch.cuda.set_device(local_rank)
-        torch.distributed.init_process_group("nccl")
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     rc = run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch

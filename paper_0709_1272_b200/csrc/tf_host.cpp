@@ -81,12 +81,13 @@ int level_of(int kind, int k, int j, int policy) {
 }
 
 // Tasks of Algorithms 1-3 in program order and their predecessor lists (a13 rules).
-void global_tasks(int alg, int p, int b, int policy, std::vector<TaskD>& tasks, std::vector<std::vector<int>>& preds) {
+void global_tasks(int alg, int p, int b, int ib, int policy, std::vector<TaskD>& tasks,
+                  std::vector<std::vector<int>>& preds) {
   std::unordered_map<uint64_t, int> id;
   id.reserve((size_t)p * p * p / 2 + 16);
   tasks.clear();
   auto add = [&](int kind, int k, int i, int j) {
-    TaskD d{kind, k, i, j, items_of(kind, b), 0, level_of(kind, k, j, policy), 0};
+    TaskD d{kind, k, i, j, items_of(kind, b, ib), 0, level_of(kind, k, j, policy), 0};
     id[key4(kind, k, i, j)] = (int)tasks.size();
     tasks.push_back(d);
   };
@@ -177,10 +178,10 @@ void finalize_dag(HostDag& G, const std::vector<std::vector<int>>& preds) {
     if (G.indeg0[t] == 0 && G.tasks[t].kind != K_RECV) G.roots.push_back(t);
 }
 
-void build_dag(HostDag& G, int alg, int p, int b, int policy) {
+void build_dag(HostDag& G, int alg, int p, int b, int ib, int policy) {
   G.alg = alg; G.p = p; G.b = b; G.policy = policy;
   std::vector<std::vector<int>> preds;
-  global_tasks(alg, p, b, policy, G.tasks, preds);
+  global_tasks(alg, p, b, ib, policy, G.tasks, preds);
   finalize_dag(G, preds);
 }
 
@@ -219,7 +220,7 @@ void build_plan(DistPlan& D, int alg, int p, int b, int ib, int P, int Q, int po
   const int R = D.nranks;
   std::vector<TaskD> gt;
   std::vector<std::vector<int>> gpred;
-  global_tasks(alg, p, b, policy, gt, gpred);
+  global_tasks(alg, p, b, ib, policy, gt, gpred);
   D.gtasks = gt;
   const int nt = (int)gt.size();
   std::vector<int> own(nt);
@@ -309,7 +310,7 @@ struct DevDag {
   SendEnt* sends = nullptr;
 };
 
-std::map<std::tuple<int, int, int, int, int>, DevDag> g_dags;  // (dev, alg, p, b, policy)
+std::map<std::tuple<int, int, int, int, int, int>, DevDag> g_dags;  // (dev, alg, p, b, ib, policy)
 
 template <class T>
 int upload(T** dst, const std::vector<T>& v) {
@@ -340,13 +341,13 @@ void free_dag(DevDag& D) {
   D = DevDag();
 }
 
-int get_dag(int dev, int alg, int p, int b, DevDag** out) {
-  auto key = std::make_tuple(dev, alg, p, b, g_policy);
+int get_dag(int dev, int alg, int p, int b, int ib, DevDag** out) {
+  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy);
   auto it = g_dags.find(key);
   if (it != g_dags.end()) { *out = &it->second; return 0; }
   DevDag D;
   D.h = std::make_shared<HostDag>();
-  build_dag(*D.h, alg, p, b, g_policy);
+  build_dag(*D.h, alg, p, b, ib, g_policy);
   int rc;
   if ((rc = upload_dag(D))) return rc;
   auto res = g_dags.emplace(key, D);
@@ -444,7 +445,7 @@ int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, dou
   if ((rc = device_setup(dev))) return rc;
   const int p = (int)(n / b);
   DevDag* D;
-  if ((rc = get_dag(dev, alg, p, (int)b, &D))) return rc;
+  if ((rc = get_dag(dev, alg, p, (int)b, (int)ib, &D))) return rc;
   const HostDag& H = *D->h;
   Workspace& W = g_ws[std::make_pair(dev, stream)];
   W.stream = stream;
@@ -801,7 +802,7 @@ int64_t tile_dag_export(int alg, int64_t p, int policy, int32_t* kind, int32_t* 
                         int64_t* nedges) {
   if (alg < 0 || alg > 2 || p <= 0) return -1;
   HostDag G;
-  build_dag(G, alg, (int)p, 128, policy);
+  build_dag(G, alg, (int)p, 128, 32, policy);
   const int64_t nt = (int64_t)G.tasks.size();
   for (int64_t t = 0; t < nt && t < cap; ++t) {
     if (kind) kind[t] = G.tasks[t].kind;
@@ -831,7 +832,7 @@ int tk_run(int kind, int64_t b, int64_t ib, double* t0, double* t1, double* t2, 
   int rc;
   if ((rc = device_setup(dev))) return rc;
   Workspace& W = g_ws[std::make_pair(dev, s)];
-  const int items = items_of(kind, (int)b);
+  const int items = items_of(kind, (int)b, (int)ib);
   const size_t scr = scr_stride_for((int)b, (int)ib);
   if ((rc = ensure(W.scratch, scr * items * sizeof(double)))) return rc;
   if ((rc = ensure(W.vx, (size_t)b * b * sizeof(double)))) return rc;

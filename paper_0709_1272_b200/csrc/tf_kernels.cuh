@@ -481,10 +481,143 @@ __device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* T
   }
 }
 
+// SSRFB, register-resident slab (the path for b in {128, 256, 512}, ib in {32, 64}):
+// item = NSR = 32 columns of [R_kj; A_ij].  Warp w keeps rows [w*RW, (w+1)*RW) of the A
+// slab (RW = b/16 = 8*MI) in DMMA accumulator registers for all t inner blocks, so A is
+// read and written once per item instead of twice per inner block.  Per block s:
+//   W  = R[s] + V_s^T A   16 rows of W per pass: each warp multiplies its rows (K = RW),
+//                         B fragments taken from its A registers by warp shuffles; the 16
+//                         partials are summed in a fixed order through shared memory
+//   W2 = T_s^T W          (scalar, smem);  R[s] -= W2
+//   A -= V_s W2           DMMA into the resident accumulators (K = ib)
+// V_s fragments are loaded straight from L2 (V_ik is final and read-only here).
+template <int MI>
+__device__ inline void ssrfb_reg(const Ctx& cx, const double* V, const double* Tst, double* R, double* A, int item,
+                                 double* sm) {
+  constexpr int RW = 8 * MI;   // rows per warp
+  constexpr int NJ = NSR / 8;  // n-blocks of the slab
+  constexpr int LDW = NSR + 4; // W / W2 row stride in smem (conflict-free B fragments)
+  const int b = cx.b, ib = cx.ib;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+  const int n0 = item * NSR;
+  R += (size_t)n0 * b;
+  A += (size_t)n0 * b;
+  const int r0 = warp * RW;
+  double* part = sm;                    // 16 x 512 partial sums (fragment order)
+  double* sW = part + TF_WARPS * 512;   // ib x LDW: W, then W2
+  double* sT = sW + 64 * LDW;           // T_s^T, ld ib+1
+  double acc[MI][NJ][2];
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) acc[i][j][e] = ldg_cg(A + (r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * b);
+  // shuffle source for B fragments: row 4*ks + q, column 8*j + g of the warp's stripe
+  const int e_sel = g & 1;
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    const double* Vs = V + (size_t)c0 * b;
+    // T_s^T into smem (overlaps the W products)
+    for (int e = tid; e < ib * ib; e += TF_THREADS) {
+      const int r = e % ib, c = e / ib;  // T_s(r, c), upper triangular
+      sT[c * (ib + 1) + r] = (r <= c) ? ldg_cg(Tst + (size_t)c0 * ib + e) : 0.0;
+    }
+    for (int ch = 0; ch < ib; ch += 16) {  // 16 rows of W per pass (register budget)
+      double pc[2][NJ][2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) pc[mi][j][0] = pc[mi][j][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < RW / 4; ++ks) {
+        double a[2], bf[NJ];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) a[mi] = Vs[(r0 + 4 * ks + q) + (size_t)(ch + 8 * mi + g) * b];
+        const int src = 16 * (ks & 1) + 4 * q + (g >> 1);
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const double v0 = __shfl_sync(0xffffffffu, acc[ks >> 1][j][0], src);
+          const double v1 = __shfl_sync(0xffffffffu, acc[ks >> 1][j][1], src);
+          bf[j] = e_sel ? v1 : v0;
+        }
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) dmma(pc[mi][j], a[mi], bf[j]);
+      }
+      double* slot = part + warp * 512;
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) slot[((mi * NJ + j) * 2 + e) * 32 + lane] = pc[mi][j][e];
+      __syncthreads();
+      {
+        const int f = tid;  // 512 outputs, one per thread
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < TF_WARPS; ++w) sum += part[w * 512 + f];
+        const int fl = f & 31, e = (f >> 5) & 1, j = (f >> 6) % NJ, mi = (f >> 6) / NJ;
+        const int m = ch + 8 * mi + (fl >> 2), c = 8 * j + 2 * (fl & 3) + e;
+        sW[m * LDW + c] = sum + ldg_cg(R + (c0 + m) + (size_t)c * b);
+      }
+      __syncthreads();
+    }
+    // W2 = T_s^T W (into registers), then R[s] -= W2 and W2 -> sW
+    double w2[(64 * NSR) / TF_THREADS];
+#pragma unroll
+    for (int x = 0; x < (64 * NSR) / TF_THREADS; ++x) {
+      const int e = tid + x * TF_THREADS;
+      w2[x] = 0.0;
+      if (e < ib * NSR) {
+        const int m = e % ib, c = e / ib;
+        double sum = 0.0;
+        for (int qq = 0; qq <= m; ++qq) sum += sT[m * (ib + 1) + qq] * sW[qq * LDW + c];
+        w2[x] = sum;
+        double* pr = R + (c0 + m) + (size_t)c * b;
+        *pr = ldg_cg(pr) - sum;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < (64 * NSR) / TF_THREADS; ++x) {
+      const int e = tid + x * TF_THREADS;
+      if (e < ib * NSR) sW[(e % ib) * LDW + e / ib] = w2[x];
+    }
+    __syncthreads();
+    // A -= V_s W2
+    for (int ks = 0; ks < ib / 4; ++ks) {
+      double a[MI], bq[NJ];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) a[i] = -Vs[(r0 + 8 * i + g) + (size_t)(4 * ks + q) * b];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) bq[j] = sW[(4 * ks + q) * LDW + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], a[i], bq[j]);
+    }
+    __syncthreads();  // sW / sT / part are rewritten by the next block
+  }
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) A[(r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * b] = acc[i][j][e];
+}
+
 // SSRFB: slab `item` of [R; A] <- Q_ik^T [R; A].
 __device__ inline void ssrfb_item(const Ctx& cx, const double* V, const double* Tst, double* R, double* A,
                                   int item, double* sm) {
   const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
+  if (ssrfb_reg_ok(b, ib)) {
+    if (b == 512) ssrfb_reg<4>(cx, V, Tst, R, A, item, sm);
+    else if (b == 256) ssrfb_reg<2>(cx, V, Tst, R, A, item, sm);
+    else ssrfb_reg<1>(cx, V, Tst, R, A, item, sm);
+    return;
+  }
   const int n0 = item * NS, nc = min(NS, b - n0);
   double* W = cx.scratch;
   double* W2 = W + (size_t)ib * b;

@@ -33,13 +33,19 @@ constexpr int K_SEND = 12, K_RECV = 13;
 
 TF_HD inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
-TF_HD inline int items_of(int kind, int b) {
+// SSRFB with the slab of A register-resident across the inner blocks (tf_kernels.cuh
+// ssrfb_reg): b a multiple of 128 up to 512, ib a multiple of 32; slabs of NSR columns.
+constexpr int NSR = 32;
+TF_HD inline bool ssrfb_reg_ok(int b, int ib) { return b % 128 == 0 && b <= 512 && ib % 32 == 0 && ib <= 64; }
+
+TF_HD inline int items_of(int kind, int b, int ib) {
   const int nr = ceil_div(b, RB);
   switch (kind) {
     case 1: return nr;                 // TRSM: row blocks
     case 2: return nr * (nr + 1) / 2;  // SYRK: lower sub-tiles
     case 3: return nr * nr;            // GEMM: sub-tiles
-    case 5: case 7: case 9: case 11: return ceil_div(b, NS);  // slabs
+    case 7: return ssrfb_reg_ok(b, ib) ? b / NSR : ceil_div(b, NS);
+    case 5: case 9: case 11: return ceil_div(b, NS);  // slabs
     default: return 1;                 // panels, RECV
   }
 }

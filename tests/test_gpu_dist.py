@@ -201,3 +201,46 @@ def test_dist_emulate_chol_not_spd_reports_info_and_stops():
     G, _, _, info = run_dist("chol", T2, n, b, ib, P, Q)
     m = lower_mask(n, b)
     assert info == 0 and torch.equal(G[m], R1[m])
+
+
+@pytest.mark.parametrize("alg", ["chol", "qr", "lu"])
+def test_dist_handle_single_rank_equals_one_gpu(alg):
+    """tile_dist_open/factor/close (the one-process-per-GPU API) with a 1 x 1 grid."""
+    n, b, ib = 1024, 128, 32
+    A = _gen(alg, n, 4)
+    T0 = gpu_pack(A, b)
+    R1, aux1, piv1, _ = one_gpu(alg, T0.clone(), n, b, ib)
+    h = tf.DistHandle(alg, n, b, ib, 1, 1, 0)
+    Aloc, aux, piv = scatter(alg, T0, n, b, ib, 1, 1)
+    info = torch.full((1,), 7, dtype=torch.int32, device="cuda")
+    for _ in range(2):  # repeated calls: epoch-tagged barriers
+        Aloc, aux, piv = scatter(alg, T0, n, b, ib, 1, 1)
+        h.factor(Aloc[0], None if aux is None else aux[0], None if piv is None else piv[0], info)
+        torch.cuda.synchronize()
+        assert int(info.item()) == 0
+        if alg == "chol":
+            m = lower_mask(n, b)
+            assert torch.equal(Aloc[0][m], R1[m])
+        else:
+            assert torch.equal(Aloc[0], R1)
+    h.close()
+
+
+def test_bench_dist_runner_single_rank():
+    """bench.py's multi-GPU runner end to end with a 1-rank process group (gloo)."""
+    import os
+    import sys
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        for c in (1, 2, 3):
+            cfg = dict(bench.CONFIGS[c])
+            res = bench.run_dist_device(tf, torch, cfg, 2, 1, 0, 1)
+            assert res["info"] == 0 and len(res["ms"]) == 2 and res["grid"] == "1x1"
+            assert res["e2e"]["h2d"] == cfg["n"] ** 2 * 8
+    finally:
+        dist.destroy_process_group()

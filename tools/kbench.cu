@@ -25,7 +25,7 @@ kb_kernel(int kind, int b, int ib, double* tiles, double* aux, int* ipiv, double
   double* t2 = t1 + bb;
   double* ax = aux + (size_t)blockIdx.x * ib * b;
   int* pv = ipiv + (size_t)blockIdx.x * b;
-  const int nit = items_of(kind, b);
+  const int nit = items_of(kind, b, ib);
   pipe_init(sm);
   for (int r = 0; r < reps; ++r) {
     const int it = (blockIdx.x + r) % nit;
@@ -108,7 +108,7 @@ int main(int argc, char** argv) {
                             4.0 * b * b * b / 3, 2.0 * b * b * b + 3.0 * ib * b * b, 2.0 * b * b * b + (double)ib * b * b,
                             4.0 * b * b * b + (double)ib * b * b, 2.0 * b * b * b / 3, (double)b * b * b,
                             (double)b * b * b + ib * (double)b * b / 2, 2.0 * b * b * b + (double)ib * b * b};
-  const double fl = fl_task[kind] / items_of(kind, b) * (double)grid * reps;
+  const double fl = fl_task[kind] / items_of(kind, b, ib) * (double)grid * reps;
   const double us_item = ms * 1e3 / reps;
   printf("{\"kind\": \"%s\", \"b\": %d, \"ib\": %d, \"grid\": %d, \"reps\": %d, \"ms\": %.3f, \"us_per_item\": %.2f, "
          "\"gflops_per_sm\": %.2f, \"tflops\": %.3f}\n",

@@ -488,24 +488,41 @@ __device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* T
 //   W  = R[s] + V_s^T A   16 rows of W per pass: each warp multiplies its rows (K = RW),
 //                         B fragments taken from its A registers by warp shuffles; the 16
 //                         partials are summed in a fixed order through shared memory
-//   W2 = T_s^T W          (scalar, smem);  R[s] -= W2
+//   W2 = T_s^T W          (DMMA, smem operands);  R[s] -= W2
 //   A -= V_s W2           DMMA into the resident accumulators (K = ib)
 // V_s fragments are loaded straight from L2 (V_ik is final and read-only here).
 template <int MI>
 __device__ inline void ssrfb_reg(const Ctx& cx, const double* V, const double* Tst, double* R, double* A, int item,
                                  double* sm) {
-  constexpr int RW = 8 * MI;   // rows per warp
-  constexpr int NJ = NSR / 8;  // n-blocks of the slab
-  constexpr int LDW = NSR + 4; // W / W2 row stride in smem (conflict-free B fragments)
+  constexpr int RW = 8 * MI;          // rows per warp
+  constexpr int NJ = NSR / 8;         // n-blocks of the slab
+  constexpr int LDW = NSR + 4;        // W / W2 row stride in smem (conflict-free B fragments)
+  constexpr int LDC = 64 + 2;         // column stride of the T_s and R[s] blocks in smem
+  constexpr int PB = TF_WARPS * 512;  // one partial-sum buffer (16 rows of W per warp)
   const int b = cx.b, ib = cx.ib;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   const int n0 = item * NSR;
   R += (size_t)n0 * b;
   A += (size_t)n0 * b;
   const int r0 = warp * RW;
-  double* part = sm;                    // 16 x 512 partial sums (fragment order)
-  double* sW = part + TF_WARPS * 512;   // ib x LDW: W, then W2
-  double* sT = sW + 64 * LDW;           // T_s^T, ld ib+1
+  double* part = sm;             // 2 x PB partial sums (fragment order), double-buffered
+  double* sW2 = sm;              // ib x LDW: W2 (aliases the partial buffers after the W passes)
+  double* sW = part + 2 * PB;    // ib x LDW: W = V_s^T A (R[s] added in the T phase)
+  double* sR = sW + 64 * LDW;    // R[s] rows of the slab, column-major, ld LDC
+  double* sT = sR + NSR * LDC;   // T_s, column-major, ld LDC (its zero lower part included)
+  // T_s and R[s] for block c0 land in smem by cp.async (one commit group)
+  auto prefetch_tr = [&](int c0) {
+    for (int x = tid; x < ib * (ib / 2); x += TF_THREADS) {  // T_s: ib columns of ib doubles
+      const int c = x / (ib / 2), r = 2 * (x % (ib / 2));
+      cp_async16(sT + c * LDC + r, Tst + (size_t)c0 * ib + (size_t)c * ib + r, 16);
+    }
+    for (int x = tid; x < NSR * (ib / 2); x += TF_THREADS) {  // R[s]: NSR columns of ib doubles
+      const int c = x / (ib / 2), r = 2 * (x % (ib / 2));
+      cp_async16(sR + c * LDC + r, R + c0 + r + (size_t)c * b, 16);
+    }
+    cp_async_commit();
+  };
+  prefetch_tr(0);
   double acc[MI][NJ][2];
 #pragma unroll
   for (int i = 0; i < MI; ++i)
@@ -513,92 +530,131 @@ __device__ inline void ssrfb_reg(const Ctx& cx, const double* V, const double* T
     for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) acc[i][j][e] = ldg_cg(A + (r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * b);
-  // shuffle source for B fragments: row 4*ks + q, column 8*j + g of the warp's stripe
-  const int e_sel = g & 1;
+  // B fragments (row 4*ks + q, column 8*j + g of the warp's rows) from the accumulators:
+  // both k-steps 2i, 2i+1 of accumulator block i in two 64-bit shuffle rounds (lanes < 16
+  // hold rows 0-3, lanes >= 16 rows 4-7 of the block; g odd wants the odd column)
+  const int src = 4 * q + (g >> 1);
+  const bool lo = lane < 16, odd = g & 1;
+  auto bpair = [&](int i, int j, double& b0, double& b1) {
+    const double s1 = __shfl_sync(0xffffffffu, lo ? acc[i][j][0] : acc[i][j][1], odd ? src + 16 : src);
+    const double s2 = __shfl_sync(0xffffffffu, lo ? acc[i][j][1] : acc[i][j][0], odd ? src : src + 16);
+    b0 = odd ? s2 : s1;  // row q     (k-step 2i)
+    b1 = odd ? s1 : s2;  // row 4 + q (k-step 2i+1)
+  };
+  auto reduce = [&](int ch, const double* buf) {
+    const int f = tid;  // 512 outputs, one per thread, fixed summation order
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < TF_WARPS; ++w) sum += buf[w * 512 + f];
+    const int fl = f & 31, e = (f >> 5) & 1, j = (f >> 6) % NJ, mi = (f >> 6) / NJ;
+    sW[(ch + 8 * mi + (fl >> 2)) * LDW + 8 * j + 2 * (fl & 3) + e] = sum;
+  };
+#ifdef TF_PROBE
+  unsigned long long t0 = probe_now();
+#endif
   for (int c0 = 0; c0 < b; c0 += ib) {
     const double* Vs = V + (size_t)c0 * b;
-    // T_s^T into smem (overlaps the W products)
-    for (int e = tid; e < ib * ib; e += TF_THREADS) {
-      const int r = e % ib, c = e / ib;  // T_s(r, c), upper triangular
-      sT[c * (ib + 1) + r] = (r <= c) ? ldg_cg(Tst + (size_t)c0 * ib + e) : 0.0;
-    }
-    for (int ch = 0; ch < ib; ch += 16) {  // 16 rows of W per pass (register budget)
+    // ---- W = V_s^T A in passes of 16 rows: partial products by warp rows, reduced one pass
+    // later (double-buffered partials, one CTA barrier per pass)
+#ifdef TF_EXP_SKIP_W
+    const int np = 1;
+#else
+    const int np = ib / 16;
+#endif
+    for (int pp = 0; pp < np; ++pp) {
+      const int ch = pp * 16;
       double pc[2][NJ][2];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int j = 0; j < NJ; ++j) pc[mi][j][0] = pc[mi][j][1] = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < RW / 4; ++ks) {
-        double a[2], bf[NJ];
+      for (int i = 0; i < MI; ++i) {
+        double a[2][2];  // [k-step parity][m-block]
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi) a[mi] = Vs[(r0 + 4 * ks + q) + (size_t)(ch + 8 * mi + g) * b];
-        const int src = 16 * (ks & 1) + 4 * q + (g >> 1);
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) a[h][mi] = Vs[(r0 + 8 * i + 4 * h + q) + (size_t)(ch + 8 * mi + g) * b];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
-          const double v0 = __shfl_sync(0xffffffffu, acc[ks >> 1][j][0], src);
-          const double v1 = __shfl_sync(0xffffffffu, acc[ks >> 1][j][1], src);
-          bf[j] = e_sel ? v1 : v0;
+          double b0, b1;
+          bpair(i, j, b0, b1);
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) {
+            dmma(pc[mi][j], a[0][mi], b0);
+            dmma(pc[mi][j], a[1][mi], b1);
+          }
         }
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-          for (int j = 0; j < NJ; ++j) dmma(pc[mi][j], a[mi], bf[j]);
+        if (i & 1) asm volatile("" ::: "memory");  // bound load hoisting (register budget)
       }
-      double* slot = part + warp * 512;
+      double* slot = part + (pp & 1) * PB + warp * 512;
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) slot[((mi * NJ + j) * 2 + e) * 32 + lane] = pc[mi][j][e];
-      __syncthreads();
-      {
-        const int f = tid;  // 512 outputs, one per thread
-        double sum = 0.0;
-#pragma unroll
-        for (int w = 0; w < TF_WARPS; ++w) sum += part[w * 512 + f];
-        const int fl = f & 31, e = (f >> 5) & 1, j = (f >> 6) % NJ, mi = (f >> 6) / NJ;
-        const int m = ch + 8 * mi + (fl >> 2), c = 8 * j + 2 * (fl & 3) + e;
-        sW[m * LDW + c] = sum + ldg_cg(R + (c0 + m) + (size_t)c * b);
-      }
+      if (pp > 0) reduce(ch - 16, part + ((pp - 1) & 1) * PB);
+      if (pp == np - 1) cp_async_wait<0>();  // this block's T_s / R[s]
       __syncthreads();
     }
-    // W2 = T_s^T W (into registers), then R[s] -= W2 and W2 -> sW
-    double w2[(64 * NSR) / TF_THREADS];
+    reduce(ib - 16, part + ((np - 1) & 1) * PB);
+    __syncthreads();
+    TF_PROBE_MARK(0, t0);
+    // ---- W2 = T_s^T (R[s] + W) on the tensor pipe.  T_s^T is lower triangular, so the 8x8
+    // output block (mi, j) needs k < 8(mi+1); warp -> row block mi, ib/32 column blocks
+    {
+      const int bpw = ib / 32;  // 8x8 blocks per warp (1 or 2), same mi
+      const int mi = warp / (NJ / bpw), j0 = (warp % (NJ / bpw)) * bpw;
+      double c2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#ifdef TF_EXP_SKIP_T
+      const int nks = 0;
+#else
+      const int nks = 2 * (mi + 1);
+#endif
+      for (int ks = 0; ks < nks; ++ks) {
+        const int k = 4 * ks + q;
+        const double a = sT[(8 * mi + g) * LDC + k];  // T_s^T(m, k) = T_s(k, m)
+        const double b0 = sW[k * LDW + 8 * j0 + g] + sR[(8 * j0 + g) * LDC + k];
+        dmma(c2[0], a, b0);
+        if (bpw == 2) {
+          const double b1 = sW[k * LDW + 8 * j0 + 8 + g] + sR[(8 * j0 + 8 + g) * LDC + k];
+          dmma(c2[1], a, b1);
+        }
+      }
 #pragma unroll
-    for (int x = 0; x < (64 * NSR) / TF_THREADS; ++x) {
-      const int e = tid + x * TF_THREADS;
-      w2[x] = 0.0;
-      if (e < ib * NSR) {
-        const int m = e % ib, c = e / ib;
-        double sum = 0.0;
-        for (int qq = 0; qq <= m; ++qq) sum += sT[m * (ib + 1) + qq] * sW[qq * LDW + c];
-        w2[x] = sum;
-        double* pr = R + (c0 + m) + (size_t)c * b;
-        *pr = ldg_cg(pr) - sum;
+      for (int x = 0; x < 2; ++x) {
+        if (x < bpw) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int m = 8 * mi + g, c = 8 * (j0 + x) + 2 * q + e;
+            sW2[m * LDW + c] = c2[x][e];
+            R[(c0 + m) + (size_t)c * b] = sR[c * LDC + m] - c2[x][e];
+          }
+        }
       }
     }
     __syncthreads();
-#pragma unroll
-    for (int x = 0; x < (64 * NSR) / TF_THREADS; ++x) {
-      const int e = tid + x * TF_THREADS;
-      if (e < ib * NSR) sW[(e % ib) * LDW + e / ib] = w2[x];
-    }
-    __syncthreads();
-    // A -= V_s W2
+    if (c0 + ib < b) prefetch_tr(c0 + ib);  // next block's T_s / R[s] (sT, sR are free now)
+    TF_PROBE_MARK(1, t0);
+    // ---- A -= V_s W2
+#ifdef TF_EXP_SKIP_U
+    for (int ks = 0; ks < 0; ++ks) {
+#else
     for (int ks = 0; ks < ib / 4; ++ks) {
+#endif
       double a[MI], bq[NJ];
 #pragma unroll
       for (int i = 0; i < MI; ++i) a[i] = -Vs[(r0 + 8 * i + g) + (size_t)(4 * ks + q) * b];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) bq[j] = sW[(4 * ks + q) * LDW + 8 * j + g];
+      for (int j = 0; j < NJ; ++j) bq[j] = sW2[(4 * ks + q) * LDW + 8 * j + g];
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < NJ; ++j) dmma(acc[i][j], a[i], bq[j]);
     }
-    __syncthreads();  // sW / sT / part are rewritten by the next block
+    __syncthreads();  // sW2 / part are rewritten by the next block
+    TF_PROBE_MARK(2, t0);
   }
 #pragma unroll
   for (int i = 0; i < MI; ++i)

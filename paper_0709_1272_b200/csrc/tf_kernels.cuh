@@ -319,7 +319,7 @@ __device__ inline void geqrt_panel(double* P, int ldp, int mp, int ib, double* T
 
 // GEQRT with inner block ib.  Writes the explicit unit-lower copy of
 // V (VX, b x b) for the LARFB items of this step.
-__device__ inline void geqrt_item(const Ctx& cx, double* A, double* Tst, double* VX, double* sm) {
+__device__ inline void geqrt_ref(const Ctx& cx, double* A, double* Tst, double* VX, double* sm) {
   const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
   double* W = cx.scratch;
   double* W2 = W + (size_t)ib * b;
@@ -369,7 +369,7 @@ __device__ inline void geqrt_item(const Ctx& cx, double* A, double* Tst, double*
 }
 
 // LARFB: slab `item` of C <- Q_kk^T C, s = 0..t-1 (reading Z5).
-__device__ inline void larfb_item(const Ctx& cx, const double* VX, const double* Tst, double* C, int item,
+__device__ inline void larfb_ref(const Ctx& cx, const double* VX, const double* Tst, double* C, int item,
                                   double* sm) {
   const int b = cx.b, ib = cx.ib;
   const int n0 = item * NS, nc = min(NS, b - n0);
@@ -391,6 +391,9 @@ __device__ inline void larfb_item(const Ctx& cx, const double* VX, const double*
 __device__ inline void tsqrt_panel(double* P, int ldp, int b, double* Rb, int ib, double* Ts, double* red,
                                    double* sdot) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef TF_PROBE
+  unsigned long long t0 = probe_now();
+#endif
   for (int jj = 0; jj < ib; ++jj) {
     double ss = 0.0;
     for (int r = tid; r < b; r += TF_THREADS) {
@@ -398,9 +401,11 @@ __device__ inline void tsqrt_panel(double* P, int ldp, int b, double* Rb, int ib
       ss += x * x;
     }
     ss = block_sum(ss, red);
+    TF_PROBE_MARK(4, t0);
     const double alpha = Rb[jj + jj * ib];
     const House h = make_house(alpha, ss);
     __syncthreads();
+    TF_PROBE_MARK(5, t0);
     if (ss != 0.0) {
       for (int r = tid; r < b; r += TF_THREADS) P[r + (size_t)jj * ldp] = P[r + (size_t)jj * ldp] / h.den;
       if (tid == 0) Rb[jj + jj * ib] = h.beta;
@@ -414,6 +419,7 @@ __device__ inline void tsqrt_panel(double* P, int ldp, int b, double* Rb, int ib
       if (lane == 0) sdot[c] = (c > jj) ? Rb[jj + c * ib] + s : s;
     }
     __syncthreads();
+    TF_PROBE_MARK(6, t0);
     const int ncol = ib - jj - 1;
     for (int e = tid; e < b * ncol; e += TF_THREADS) {
       const int r = e % b, c = jj + 1 + e / b;
@@ -427,15 +433,19 @@ __device__ inline void tsqrt_panel(double* P, int ldp, int b, double* Rb, int ib
     }
     if (tid == 0) Ts[jj + jj * ib] = h.tau;
     __syncthreads();
+    TF_PROBE_MARK(7, t0);
   }
 }
 
 // TSQRT (inner blocking PAPER.md:637-647): QR of [R; A].  Reads and
 // writes only the upper region of the diagonal tile R.
-__device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* Tst, double* sm) {
+__device__ inline void tsqrt_ref(const Ctx& cx, double* R, double* A, double* Tst, double* sm) {
   const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
   double* W = cx.scratch;
   double* W2 = W + (size_t)ib * b;
+#ifdef TF_PROBE
+  unsigned long long t0 = probe_now();
+#endif
   for (int c0 = 0; c0 < b; c0 += ib) {
     const int c1 = c0 + ib;
     double* Ts = sm;
@@ -456,7 +466,9 @@ __device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* T
       P = A + (size_t)c0 * b;
     }
     __syncthreads();
+    TF_PROBE_MARK(3, t0);
     tsqrt_panel(P, ldp, b, Rb, ib, Ts, red, sdot);
+    TF_PROBE_MARK(0, t0);
     if (in_smem)
       for (int e = tid; e < b * ib; e += TF_THREADS) A[(size_t)c0 * b + e] = P[e];
     for (int e = tid; e < ib * ib; e += TF_THREADS) {
@@ -468,6 +480,7 @@ __device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* T
     if (c1 < b) {
       // W = R[c0:c1, c1:b] + V_s^T A[:, c1:b]; W2 = T_s^T W; R -= W2; A[:, c1:b] -= V_s W2
       w_product(sm, W, ib, A + (size_t)c0 * b, b, A + (size_t)c1 * b, b, ib, b - c1, b, R + c0 + (size_t)c1 * b, b);
+      TF_PROBE_MARK(1, t0);
       load_ts(sm, Tst, ib, c0);
       apply_tt(sm, ib, W, W2, ib, b - c1);
       for (int e = tid; e < ib * (b - c1); e += TF_THREADS) {
@@ -477,203 +490,16 @@ __device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* T
       }
       update_mn(sm, A + (size_t)c1 * b, b, A + (size_t)c0 * b, b, W2, ib, b, b - c1, ib);
       __syncthreads();
+      TF_PROBE_MARK(2, t0);
     }
   }
 }
 
-// SSRFB, register-resident slab (the path for b in {128, 256, 512}, ib in {32, 64}):
-// item = NSR = 32 columns of [R_kj; A_ij].  Warp w keeps rows [w*RW, (w+1)*RW) of the A
-// slab (RW = b/16 = 8*MI) in DMMA accumulator registers for all t inner blocks, so A is
-// read and written once per item instead of twice per inner block.  Per block s:
-//   W  = R[s] + V_s^T A   16 rows of W per pass: each warp multiplies its rows (K = RW),
-//                         B fragments taken from its A registers by warp shuffles; the 16
-//                         partials are summed in a fixed order through shared memory
-//   W2 = T_s^T W          (DMMA, smem operands);  R[s] -= W2
-//   A -= V_s W2           DMMA into the resident accumulators (K = ib)
-// V_s fragments are loaded straight from L2 (V_ik is final and read-only here).
-template <int MI>
-__device__ inline void ssrfb_reg(const Ctx& cx, const double* V, const double* Tst, double* R, double* A, int item,
-                                 double* sm) {
-  constexpr int RW = 8 * MI;          // rows per warp
-  constexpr int NJ = NSR / 8;         // n-blocks of the slab
-  constexpr int LDW = NSR + 4;        // W / W2 row stride in smem (conflict-free B fragments)
-  constexpr int LDC = 64 + 2;         // column stride of the T_s and R[s] blocks in smem
-  constexpr int PB = TF_WARPS * 512;  // one partial-sum buffer (16 rows of W per warp)
-  const int b = cx.b, ib = cx.ib;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
-  const int n0 = item * NSR;
-  R += (size_t)n0 * b;
-  A += (size_t)n0 * b;
-  const int r0 = warp * RW;
-  double* part = sm;             // 2 x PB partial sums (fragment order), double-buffered
-  double* sW2 = sm;              // ib x LDW: W2 (aliases the partial buffers after the W passes)
-  double* sW = part + 2 * PB;    // ib x LDW: W = V_s^T A (R[s] added in the T phase)
-  double* sR = sW + 64 * LDW;    // R[s] rows of the slab, column-major, ld LDC
-  double* sT = sR + NSR * LDC;   // T_s, column-major, ld LDC (its zero lower part included)
-  // T_s and R[s] for block c0 land in smem by cp.async (one commit group)
-  auto prefetch_tr = [&](int c0) {
-    for (int x = tid; x < ib * (ib / 2); x += TF_THREADS) {  // T_s: ib columns of ib doubles
-      const int c = x / (ib / 2), r = 2 * (x % (ib / 2));
-      cp_async16(sT + c * LDC + r, Tst + (size_t)c0 * ib + (size_t)c * ib + r, 16);
-    }
-    for (int x = tid; x < NSR * (ib / 2); x += TF_THREADS) {  // R[s]: NSR columns of ib doubles
-      const int c = x / (ib / 2), r = 2 * (x % (ib / 2));
-      cp_async16(sR + c * LDC + r, R + c0 + r + (size_t)c * b, 16);
-    }
-    cp_async_commit();
-  };
-  prefetch_tr(0);
-  double acc[MI][NJ][2];
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NJ; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) acc[i][j][e] = ldg_cg(A + (r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * b);
-  // B fragments (row 4*ks + q, column 8*j + g of the warp's rows) from the accumulators:
-  // both k-steps 2i, 2i+1 of accumulator block i in two 64-bit shuffle rounds (lanes < 16
-  // hold rows 0-3, lanes >= 16 rows 4-7 of the block; g odd wants the odd column)
-  const int src = 4 * q + (g >> 1);
-  const bool lo = lane < 16, odd = g & 1;
-  auto bpair = [&](int i, int j, double& b0, double& b1) {
-    const double s1 = __shfl_sync(0xffffffffu, lo ? acc[i][j][0] : acc[i][j][1], odd ? src + 16 : src);
-    const double s2 = __shfl_sync(0xffffffffu, lo ? acc[i][j][1] : acc[i][j][0], odd ? src : src + 16);
-    b0 = odd ? s2 : s1;  // row q     (k-step 2i)
-    b1 = odd ? s1 : s2;  // row 4 + q (k-step 2i+1)
-  };
-  auto reduce = [&](int ch, const double* buf) {
-    const int f = tid;  // 512 outputs, one per thread, fixed summation order
-    double sum = 0.0;
-#pragma unroll
-    for (int w = 0; w < TF_WARPS; ++w) sum += buf[w * 512 + f];
-    const int fl = f & 31, e = (f >> 5) & 1, j = (f >> 6) % NJ, mi = (f >> 6) / NJ;
-    sW[(ch + 8 * mi + (fl >> 2)) * LDW + 8 * j + 2 * (fl & 3) + e] = sum;
-  };
-#ifdef TF_PROBE
-  unsigned long long t0 = probe_now();
-#endif
-  for (int c0 = 0; c0 < b; c0 += ib) {
-    const double* Vs = V + (size_t)c0 * b;
-    // ---- W = V_s^T A in passes of 16 rows: partial products by warp rows, reduced one pass
-    // later (double-buffered partials, one CTA barrier per pass)
-#ifdef TF_EXP_SKIP_W
-    const int np = 1;
-#else
-    const int np = ib / 16;
-#endif
-    for (int pp = 0; pp < np; ++pp) {
-      const int ch = pp * 16;
-      double pc[2][NJ][2];
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) pc[mi][j][0] = pc[mi][j][1] = 0.0;
-#pragma unroll
-      for (int i = 0; i < MI; ++i) {
-        double a[2][2];  // [k-step parity][m-block]
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int mi = 0; mi < 2; ++mi) a[h][mi] = Vs[(r0 + 8 * i + 4 * h + q) + (size_t)(ch + 8 * mi + g) * b];
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          double b0, b1;
-          bpair(i, j, b0, b1);
-#pragma unroll
-          for (int mi = 0; mi < 2; ++mi) {
-            dmma(pc[mi][j], a[0][mi], b0);
-            dmma(pc[mi][j], a[1][mi], b1);
-          }
-        }
-        if (i & 1) asm volatile("" ::: "memory");  // bound load hoisting (register budget)
-      }
-      double* slot = part + (pp & 1) * PB + warp * 512;
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) slot[((mi * NJ + j) * 2 + e) * 32 + lane] = pc[mi][j][e];
-      if (pp > 0) reduce(ch - 16, part + ((pp - 1) & 1) * PB);
-      if (pp == np - 1) cp_async_wait<0>();  // this block's T_s / R[s]
-      __syncthreads();
-    }
-    reduce(ib - 16, part + ((np - 1) & 1) * PB);
-    __syncthreads();
-    TF_PROBE_MARK(0, t0);
-    // ---- W2 = T_s^T (R[s] + W) on the tensor pipe.  T_s^T is lower triangular, so the 8x8
-    // output block (mi, j) needs k < 8(mi+1); warp -> row block mi, ib/32 column blocks
-    {
-      const int bpw = ib / 32;  // 8x8 blocks per warp (1 or 2), same mi
-      const int mi = warp / (NJ / bpw), j0 = (warp % (NJ / bpw)) * bpw;
-      double c2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#ifdef TF_EXP_SKIP_T
-      const int nks = 0;
-#else
-      const int nks = 2 * (mi + 1);
-#endif
-      for (int ks = 0; ks < nks; ++ks) {
-        const int k = 4 * ks + q;
-        const double a = sT[(8 * mi + g) * LDC + k];  // T_s^T(m, k) = T_s(k, m)
-        const double b0 = sW[k * LDW + 8 * j0 + g] + sR[(8 * j0 + g) * LDC + k];
-        dmma(c2[0], a, b0);
-        if (bpw == 2) {
-          const double b1 = sW[k * LDW + 8 * j0 + 8 + g] + sR[(8 * j0 + 8 + g) * LDC + k];
-          dmma(c2[1], a, b1);
-        }
-      }
-#pragma unroll
-      for (int x = 0; x < 2; ++x) {
-        if (x < bpw) {
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int m = 8 * mi + g, c = 8 * (j0 + x) + 2 * q + e;
-            sW2[m * LDW + c] = c2[x][e];
-            R[(c0 + m) + (size_t)c * b] = sR[c * LDC + m] - c2[x][e];
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (c0 + ib < b) prefetch_tr(c0 + ib);  // next block's T_s / R[s] (sT, sR are free now)
-    TF_PROBE_MARK(1, t0);
-    // ---- A -= V_s W2
-#ifdef TF_EXP_SKIP_U
-    for (int ks = 0; ks < 0; ++ks) {
-#else
-    for (int ks = 0; ks < ib / 4; ++ks) {
-#endif
-      double a[MI], bq[NJ];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) a[i] = -Vs[(r0 + 8 * i + g) + (size_t)(4 * ks + q) * b];
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) bq[j] = sW2[(4 * ks + q) * LDW + 8 * j + g];
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], a[i], bq[j]);
-    }
-    __syncthreads();  // sW2 / part are rewritten by the next block
-    TF_PROBE_MARK(2, t0);
-  }
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NJ; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) A[(r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * b] = acc[i][j][e];
-}
-
-// SSRFB: slab `item` of [R; A] <- Q_ik^T [R; A].
-__device__ inline void ssrfb_item(const Ctx& cx, const double* V, const double* Tst, double* R, double* A,
-                                  int item, double* sm) {
+// SSRFB reference-blocked path: slab `item` of
+// [R; A] <- Q_ik^T [R; A] (tile sizes the register-slab kernels do not cover).
+__device__ inline void ssrfb_ref(const Ctx& cx, const double* V, const double* Tst, double* R, double* A,
+                                 int item, double* sm) {
   const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
-  if (ssrfb_reg_ok(b, ib)) {
-    if (b == 512) ssrfb_reg<4>(cx, V, Tst, R, A, item, sm);
-    else if (b == 256) ssrfb_reg<2>(cx, V, Tst, R, A, item, sm);
-    else ssrfb_reg<1>(cx, V, Tst, R, A, item, sm);
-    return;
-  }
   const int n0 = item * NS, nc = min(NS, b - n0);
   double* W = cx.scratch;
   double* W2 = W + (size_t)ib * b;
@@ -691,6 +517,42 @@ __device__ inline void ssrfb_item(const Ctx& cx, const double* V, const double* 
     update_mn(sm, A, b, V + (size_t)c0 * b, b, W2, ib, b, nc, ib);
     __syncthreads();
   }
+}
+
+}  // namespace tf
+#include "tf_qr_slab.cuh"
+namespace tf {
+
+// QR task kernels: the register-slab path for b in {128, 256, 512} and ib in {32, 64}
+// (ssrfb_reg_ok), the reference-blocked kernels otherwise.
+#define TF_SLAB_DISPATCH(fn, ...)                      \
+  do {                                                 \
+    if (cx.b == 512) fn<4>(__VA_ARGS__);               \
+    else if (cx.b == 256) fn<2>(__VA_ARGS__);          \
+    else fn<1>(__VA_ARGS__);                           \
+  } while (0)
+
+// GEQRT: A_kk -> V_kk, R_kk, T_kk; writes the unit-lower V copy VX.
+__device__ inline void geqrt_item(const Ctx& cx, double* A, double* Tst, double* VX, double* sm) {
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(qr_slab, cx, false, A, nullptr, Tst, VX, sm);
+  else geqrt_ref(cx, A, Tst, VX, sm);
+}
+// LARFB: slab `item` of C <- Q_kk^T C.
+__device__ inline void larfb_item(const Ctx& cx, const double* VX, const double* Tst, double* C, int item,
+                                  double* sm) {
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(larfb_reg, cx, VX, Tst, C, item, sm);
+  else larfb_ref(cx, VX, Tst, C, item, sm);
+}
+// TSQRT: QR of [R_kk; A_ik]; only the upper region of R_kk is touched.
+__device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* Tst, double* sm) {
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(qr_slab, cx, true, A, R, Tst, nullptr, sm);
+  else tsqrt_ref(cx, R, A, Tst, sm);
+}
+// SSRFB: slab `item` of [R_kj; A_ij] <- Q_ik^T [R_kj; A_ij].
+__device__ inline void ssrfb_item(const Ctx& cx, const double* V, const double* Tst, double* R, double* A,
+                                  int item, double* sm) {
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(ssrfb_reg, cx, V, Tst, R, A, item, sm);
+  else ssrfb_ref(cx, V, Tst, R, A, item, sm);
 }
 
 // ====================================================================================

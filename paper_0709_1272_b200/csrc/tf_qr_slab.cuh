@@ -1,0 +1,432 @@
+// tf_qr_slab.cuh — register-resident slab kernels for tiled QR on sm_100a (b = 128, 256,
+// 512; ib = 32 or 64).  One work item owns a 32-column slab of a tile held in FP64 DMMA
+// accumulator registers (warp w: rows [w*RW, (w+1)*RW), RW = b/16), and applies whole
+// inner blocks of compact-WY reflectors to it without re-reading the slab:
+//
+//   slab_apply   [R_s; A] <- (I - Y_s T_s^T Y_s^T) [R_s; A]  (Y_s = [I; V_s] or the explicit
+//                unit-lower V_s), PAPER.md:383 / 424-427 with inner blocking (reading Z5):
+//                W = R_s + V_s^T A  (per-warp-rows DMMA partials, fixed-order reduction),
+//                W2 = T_s^T W (DMMA), R_s -= W2, A -= V_s W2 (DMMA into the resident slab)
+//   ssrfb_reg    SSRFB item = slab_apply for s = 0..t-1
+//   larfb_reg    LARFB item = slab_apply with V = V_kk copy
+//   qr_slab      GEQRT / TSQRT, left-looking over 32-column slabs (PAPER.md:358-374,
+//                386-406, inner blocking 637-647): apply every finished reflector group to
+//                the slab, then Householder-factor the slab in shared memory with one
+//                reduction (all column dots + the norm fused) and two CTA barriers per
+//                column; T blocks by the column recurrence, and for ib = 64 the coupling
+//                block T12 = -T11 (V1^T V2) T22 of the two 32-column halves.
+//
+// The arithmetic is the paper's Householder / compact-WY algorithm; only its blocking
+// and summation order differ from the oracle (parity to rounding).
+#pragma once
+#include "tf_gemm.cuh"
+#include "tf_sched.h"
+
+namespace tf {
+
+constexpr int SNJ = NSR / 8;            // n-blocks of a 32-column slab
+constexpr int SLDW = NSR + 4;           // W / W2 row stride in smem (conflict-free B fragments)
+constexpr int SLDC = 64 + 2;            // column stride of the T and R blocks in smem
+constexpr int SPB = TF_WARPS * 512;     // one partial-sum buffer (16 rows of W per warp)
+
+// [R_s; A_slab] <- Q_s^T [R_s; A_slab] for one reflector group of nw (32 or 64) columns.
+//   acc : the slab (rows r0 + 8i + g, columns 8j + 2q + e), updated in place
+//   Vs  : V column 0 of the group, (r, m) at Vs[r + m*b]; rows < vrow0 are zero and skipped
+//   Rr  : R_s rows of the slab, (m, c) at Rr[m + c*b], or null (V has its own unit diagonal)
+//   Tb  : T block of the group, (r, c) at Tb[r + c*ldt], upper triangular incl. zero lower part
+template <int MI>
+__device__ __forceinline__ void slab_apply(double (&acc)[MI][SNJ][2], const double* Vs, int vrow0, double* Rr,
+                                           const double* Tb, int nw, int ldt, int b, double* sm) {
+  constexpr int RW = 8 * MI;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+  const int r0 = warp * RW;
+  const bool active = r0 + RW > vrow0;  // this warp's rows meet V
+  double* part = sm;                 // 2 x SPB partials (fragment order), double-buffered
+  double* sW2 = sm;                  // nw x SLDW (aliases the partials after the W passes)
+  double* sW = part + 2 * SPB;       // nw x SLDW
+  double* sR = sW + 64 * SLDW;       // R_s, column-major, ld SLDC
+  double* sT = sR + NSR * SLDC;      // T, column-major, ld SLDC
+  // T and R_s land in smem by cp.async while the W passes run
+  for (int x = tid; x < nw * (nw / 2); x += TF_THREADS) {
+    const int c = x / (nw / 2), r = 2 * (x % (nw / 2));
+    cp_async16(sT + c * SLDC + r, Tb + (size_t)c * ldt + r, 16);
+  }
+  if (Rr) {
+    for (int x = tid; x < NSR * (nw / 2); x += TF_THREADS) {
+      const int c = x / (nw / 2), r = 2 * (x % (nw / 2));
+      cp_async16(sR + c * SLDC + r, Rr + r + (size_t)c * b, 16);
+    }
+  }
+  cp_async_commit();
+  // B fragments (row 4*ks + q, column 8*j + g of the warp's rows) from the accumulators:
+  // k-steps 2i, 2i+1 of accumulator block i in two 64-bit shuffle rounds
+  const int src = 4 * q + (g >> 1);
+  const bool lo = lane < 16, odd = g & 1;
+  auto bpair = [&](int i, int j, double& b0, double& b1) {
+    const double s1 = __shfl_sync(0xffffffffu, lo ? acc[i][j][0] : acc[i][j][1], odd ? src + 16 : src);
+    const double s2 = __shfl_sync(0xffffffffu, lo ? acc[i][j][1] : acc[i][j][0], odd ? src : src + 16);
+    b0 = odd ? s2 : s1;
+    b1 = odd ? s1 : s2;
+  };
+  auto reduce = [&](int ch, const double* buf) {
+    const int f = tid;  // 512 outputs, one per thread, fixed summation order
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < TF_WARPS; ++w) sum += buf[w * 512 + f];
+    const int fl = f & 31, e = (f >> 5) & 1, j = (f >> 6) % SNJ, mi = (f >> 6) / SNJ;
+    sW[(ch + 8 * mi + (fl >> 2)) * SLDW + 8 * j + 2 * (fl & 3) + e] = sum;
+  };
+  // ---- W = V^T A in passes of 16 rows (one CTA barrier per pass)
+  const int np = nw / 16;
+  for (int pp = 0; pp < np; ++pp) {
+    const int ch = pp * 16;
+    double pc[2][SNJ][2];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j) pc[mi][j][0] = pc[mi][j][1] = 0.0;
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        double a[2][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) a[h][mi] = Vs[(r0 + 8 * i + 4 * h + q) + (size_t)(ch + 8 * mi + g) * b];
+#pragma unroll
+        for (int j = 0; j < SNJ; ++j) {
+          double b0, b1;
+          bpair(i, j, b0, b1);
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) {
+            dmma(pc[mi][j], a[0][mi], b0);
+            dmma(pc[mi][j], a[1][mi], b1);
+          }
+        }
+        if (i & 1) asm volatile("" ::: "memory");  // bound load hoisting (register budget)
+      }
+    }
+    double* slot = part + (pp & 1) * SPB + warp * 512;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) slot[((mi * SNJ + j) * 2 + e) * 32 + lane] = pc[mi][j][e];
+    if (pp > 0) reduce(ch - 16, part + ((pp - 1) & 1) * SPB);
+    if (pp == np - 1) cp_async_wait<0>();
+    __syncthreads();
+  }
+  reduce(nw - 16, part + ((np - 1) & 1) * SPB);
+  __syncthreads();
+  // ---- W2 = T^T (R_s + W): T^T lower triangular -> block (mi, j) needs k < 8(mi+1)
+  {
+    const int bpw = nw / 32;  // 8x8 output blocks per warp (1 or 2), same mi
+    const int mi = warp / (SNJ / bpw), j0 = (warp % (SNJ / bpw)) * bpw;
+    double c2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const int nks = 2 * (mi + 1);
+    for (int ks = 0; ks < nks; ++ks) {
+      const int k = 4 * ks + q;
+      const double a = sT[(8 * mi + g) * SLDC + k];  // T^T(m, k) = T(k, m)
+      double b0 = sW[k * SLDW + 8 * j0 + g];
+      if (Rr) b0 += sR[(8 * j0 + g) * SLDC + k];
+      dmma(c2[0], a, b0);
+      if (bpw == 2) {
+        double b1 = sW[k * SLDW + 8 * j0 + 8 + g];
+        if (Rr) b1 += sR[(8 * j0 + 8 + g) * SLDC + k];
+        dmma(c2[1], a, b1);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      if (x < bpw) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = 8 * mi + g, c = 8 * (j0 + x) + 2 * q + e;
+          sW2[m * SLDW + c] = c2[x][e];
+          if (Rr) Rr[m + (size_t)c * b] = sR[c * SLDC + m] - c2[x][e];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- A -= V W2
+  if (active) {
+    for (int ks = 0; ks < nw / 4; ++ks) {
+      double a[MI], bq[SNJ];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) a[i] = -Vs[(r0 + 8 * i + g) + (size_t)(4 * ks + q) * b];
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j) bq[j] = sW2[(4 * ks + q) * SLDW + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < SNJ; ++j) dmma(acc[i][j], a[i], bq[j]);
+    }
+  }
+  __syncthreads();  // sW2 / sT / sR / partials are rewritten by the next group
+}
+
+template <int MI>
+__device__ __forceinline__ void slab_load(double (&acc)[MI][SNJ][2], const double* A, int b) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+  const int r0 = warp * 8 * MI;
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < SNJ; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) acc[i][j][e] = ldg_cg(A + (r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * b);
+}
+
+template <int MI>
+__device__ __forceinline__ void slab_store(const double (&acc)[MI][SNJ][2], double* A, int b) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, q = lane & 3;
+  const int r0 = warp * 8 * MI;
+#pragma unroll
+  for (int i = 0; i < MI; ++i)
+#pragma unroll
+    for (int j = 0; j < SNJ; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) A[(r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * b] = acc[i][j][e];
+}
+
+// SSRFB item: 32 columns of [R_kj; A_ij] <- Q_ik^T [R_kj; A_ij], blocks s = 0..t-1.
+template <int MI>
+__device__ inline void ssrfb_reg(const Ctx& cx, const double* V, const double* Tst, double* R, double* A, int item,
+                                 double* sm) {
+  const int b = cx.b, ib = cx.ib;
+  R += (size_t)item * NSR * b;
+  A += (size_t)item * NSR * b;
+  double acc[MI][SNJ][2];
+  slab_load<MI>(acc, A, b);
+  for (int c0 = 0; c0 < b; c0 += ib) slab_apply<MI>(acc, V + (size_t)c0 * b, 0, R + c0, Tst + (size_t)c0 * ib, ib, ib, b, sm);
+  slab_store<MI>(acc, A, b);
+}
+
+// LARFB item: 32 columns of A_kj <- Q_kk^T A_kj with the explicit unit-lower V_kk copy VX.
+template <int MI>
+__device__ inline void larfb_reg(const Ctx& cx, const double* VX, const double* Tst, double* C, int item,
+                                 double* sm) {
+  const int b = cx.b, ib = cx.ib;
+  C += (size_t)item * NSR * b;
+  double acc[MI][SNJ][2];
+  slab_load<MI>(acc, C, b);
+  for (int c0 = 0; c0 < b; c0 += ib)
+    slab_apply<MI>(acc, VX + (size_t)c0 * b, c0, nullptr, Tst + (size_t)c0 * ib, ib, ib, b, sm);
+  slab_store<MI>(acc, C, b);
+}
+
+// Householder factorization of one 32-column slab held in shared memory (P, b x 32,
+// column-major, ld ldp), column by column (PAPER.md:362-372 / 390-404).
+//   ts   : TSQRT — reflector rows are all b rows of P, the top element of each reflector
+//          is the diagonal of Rb (32 x 32, ld 33, upper part = R rows/cols of the slab),
+//          whose rows receive the top components of the updates.
+//   !ts  : GEQRT — column jj's reflector covers rows > cs + jj of P; row cs + jj is the top.
+// Thread layout: TPR = 4/MI threads per row, each owning CPT = 8*MI contiguous columns;
+// lane = u*CPT + rr (row w*CPT + rr, columns [u*CPT, (u+1)*CPT)).  Per column: the dots of
+// column jj with all 32 columns (the norm included) in one reduce-scatter + cross-warp
+// sum; warp 0 then forms the Householder scalars, the top-row updates and the T column.
+template <int MI>
+__device__ inline void slab_panel(bool ts, double* P, int ldp, int cs, double* Rb, double* Ts, double* sm2) {
+  constexpr int CPT = 8 * MI, TPR = 32 / CPT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int u = lane / CPT, rr = lane % CPT, r = warp * CPT + rr, cb = u * CPT;
+  double* part = sm2;          // 2 x 16 x 32 warp partials
+  double* sD = part + 1024;    // 32 column sums
+  double* sWc = sD + 32;       // 32: w_c
+  double* sH = sWc + 32;       // tau, den
+  (void)TPR;
+  for (int e = tid; e < 32 * 33; e += TF_THREADS) Ts[e] = 0.0;
+  __syncthreads();
+  for (int jj = 0; jj < 32; ++jj) {
+    const int cg = cs + jj;
+    const bool refl = ts || (r > cg);
+    const double x = refl ? P[r + (size_t)jj * ldp] : 0.0;
+    double v[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) v[k] = x * P[r + (size_t)(cb + k) * ldp];
+    // reduce-scatter over the CPT lanes of this column group: lane keeps column cb + rr
+#pragma unroll
+    for (int m = CPT / 2, n = CPT; m >= 1; m >>= 1, n >>= 1) {
+      const bool up = lane & m;
+#pragma unroll
+      for (int k = 0; k < n / 2; ++k) {
+        const double send = up ? v[k] : v[k + n / 2];
+        const double keep = up ? v[k + n / 2] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      }
+    }
+    double* pb = part + (jj & 1) * 512;
+    pb[warp * 32 + cb + rr] = v[0];
+    __syncthreads();
+    if (warp == 0) {
+      const int c = lane;
+      double d = 0.0;
+#pragma unroll
+      for (int w = 0; w < TF_WARPS; ++w) d += pb[w * 32 + c];
+      const double ss = __shfl_sync(0xffffffffu, d, jj);
+      const double alpha = ts ? Rb[jj * 33 + jj] : P[cg + (size_t)jj * ldp];
+      const House h = make_house(alpha, ss);
+      // sdot_c = top_c + (column jj / den) . column c: w_c for c > jj, V^T v for c < jj
+      const double top = ts ? (c > jj ? Rb[jj * 33 + c] : 0.0) : (c != jj ? P[cg + (size_t)c * ldp] : 0.0);
+      const double sdot = top + d / h.den;
+      if (c > jj) {
+        sWc[c] = sdot;
+        if (ts) Rb[jj * 33 + c] = top - h.tau * sdot;
+        else P[cg + (size_t)c * ldp] = top - h.tau * sdot;
+      }
+      if (c == jj) {
+        if (ts) Rb[jj * 33 + jj] = h.beta;
+        else P[cg + (size_t)jj * ldp] = h.beta;
+        sH[0] = h.tau;
+        sH[1] = h.den;
+      }
+      // T column jj: T[m][jj] = sum_{m' < jj} T[m][m'] (-tau sdot_m'), T[jj][jj] = tau
+      double tcol = 0.0;
+      for (int mp = 0; mp < jj; ++mp) {
+        const double s_m = __shfl_sync(0xffffffffu, sdot, mp);
+        if (c < jj) tcol += Ts[c * 33 + mp] * (-h.tau * s_m);
+      }
+      if (c < jj) Ts[c * 33 + jj] = tcol;
+      if (c == jj) Ts[jj * 33 + jj] = h.tau;
+    }
+    __syncthreads();
+    const double tau = sH[0], den = sH[1];
+    if (refl) {
+      const double vr = x / den;
+      if (jj >= cb && jj < cb + CPT) P[r + (size_t)jj * ldp] = vr;
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const int c = cb + k;
+        if (c > jj) P[r + (size_t)c * ldp] -= (tau * sWc[c]) * vr;
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+// GEQRT (ts = false: A = the diagonal tile, R unused, VX = explicit unit-lower V copy)
+// or TSQRT (ts = true: R = the diagonal tile's upper region, A = the tile below, VX unused),
+// left-looking over 32-column slabs.  Tst: the T strip (ib x b).
+template <int MI>
+__device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, double* Tst, double* VX, double* sm) {
+  const int b = cx.b, ib = cx.ib;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+  constexpr int RW = 8 * MI;
+  const int r0 = warp * RW;
+  const int ldp = b + 4;
+  const double* Vsrc = ts ? A : VX;
+  double acc[MI][SNJ][2];
+  for (int cs = 0; cs < b; cs += NSR) {
+    const int t = cs / NSR;
+    slab_load<MI>(acc, A + (size_t)cs * b, b);
+    // every finished reflector group, in order
+    for (int c0 = 0; c0 + ib <= cs; c0 += ib)
+      slab_apply<MI>(acc, Vsrc + (size_t)c0 * b, ts ? 0 : c0, ts ? R + c0 + (size_t)cs * b : nullptr,
+                     Tst + (size_t)c0 * ib, ib, ib, b, sm);
+    if (ib == 64 && (t & 1))  // first half of this inner block (T11 is its T)
+      slab_apply<MI>(acc, Vsrc + (size_t)(cs - 32) * b, ts ? 0 : cs - 32, ts ? R + (cs - 32) + (size_t)cs * b : nullptr,
+                     Tst + (size_t)(cs - 32) * ib, 32, ib, b, sm);
+    // ---- panel in shared memory
+    double* P = sm;                              // b x 32, ld ldp
+    double* Rb = P + 32 * ldp;                   // 32 x 33 (TSQRT)
+    double* Ts = Rb + 32 * 33;                   // 32 x 33, Ts[m*33 + c] = T(m, c)
+    double* sm2 = Ts + 32 * 33;                  // panel scratch (1024 + 96)
+    double* mpart = sm2 + 1152;                  // 16 x 256 (T12 products)
+    double* sM = mpart + 4096;                   // 32 x 33
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) P[(r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * ldp] = acc[i][j][e];
+    if (ts)
+      for (int e = tid; e < 32 * 32; e += TF_THREADS) {
+        const int rr = e % 32, c = e / 32;
+        Rb[rr * 33 + c] = (rr <= c) ? ldg_cg(R + (cs + rr) + (size_t)(cs + c) * b) : 0.0;
+      }
+    __syncthreads();
+    slab_panel<MI>(ts, P, ldp, cs, Rb, Ts, sm2);
+    // ---- results: the slab, R block (TSQRT), V copy (GEQRT), T block(s)
+    for (int e = tid; e < b * 32; e += TF_THREADS) {
+      const int rr = e % b, c = e / b;
+      const double pv = P[rr + (size_t)c * ldp];
+      A[rr + (size_t)(cs + c) * b] = pv;
+      if (!ts) VX[rr + (size_t)(cs + c) * b] = rr > cs + c ? pv : (rr == cs + c ? 1.0 : 0.0);
+    }
+    if (ts)
+      for (int e = tid; e < 32 * 32; e += TF_THREADS) {
+        const int rr = e % 32, c = e / 32;
+        if (rr <= c) R[(cs + rr) + (size_t)(cs + c) * b] = Rb[rr * 33 + c];
+      }
+    const int s0 = (cs / ib) * ib;       // first column of this slab's inner block
+    const int off = cs - s0;             // 0, or 32 for the second half of a 64-block
+    for (int e = tid; e < 32 * 32; e += TF_THREADS) {
+      const int rr = e % 32, c = e / 32;
+      Tst[(size_t)(cs + c) * ib + off + rr] = Ts[rr * 33 + c];  // T(off + rr, off + c)
+      if (ib == 64 && off == 0) Tst[(size_t)(cs + c) * ib + 32 + rr] = 0.0;  // T(32 + rr, c) = 0
+    }
+    if (ib == 64 && off == 32) {
+      // T12 = -T11 (V1^T V2) T22; V1 = the block's first 32 columns, V2 = this slab
+      const double* V1 = Vsrc + (size_t)(cs - 32) * b;
+      for (int pass = 0; pass < 4; ++pass) {  // 8 rows of M = V1^T V2 per pass
+        double pc[SNJ][2];
+#pragma unroll
+        for (int j = 0; j < SNJ; ++j) pc[j][0] = pc[j][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < RW / 4; ++ks) {
+          const int rw = r0 + 4 * ks + q;
+          const double a = V1[rw + (size_t)(8 * pass + g) * b];
+#pragma unroll
+          for (int j = 0; j < SNJ; ++j) {
+            const int c = 8 * j + g;
+            double bv = P[rw + (size_t)c * ldp];
+            if (!ts) bv = rw > cs + c ? bv : (rw == cs + c ? 1.0 : 0.0);
+            dmma(pc[j], a, bv);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < SNJ; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) mpart[warp * 256 + (j * 2 + e) * 32 + lane] = pc[j][e];
+        __syncthreads();
+        if (tid < 256) {
+          double sum = 0.0;
+#pragma unroll
+          for (int w = 0; w < TF_WARPS; ++w) sum += mpart[w * 256 + tid];
+          const int fl = tid & 31, e = (tid >> 5) & 1, j = tid >> 6;
+          sM[(8 * pass + (fl >> 2)) * 33 + 8 * j + 2 * (fl & 3) + e] = sum;
+        }
+        __syncthreads();
+      }
+      // tmp = M T22 (T22 upper: k <= c), then T12 = -T11 tmp (T11 upper: m >= r)
+      double tv[2];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int e = tid + x * TF_THREADS, m = e % 32, c = e / 32;
+        double s = 0.0;
+        for (int k = 0; k <= c; ++k) s += sM[m * 33 + k] * Ts[k * 33 + c];
+        tv[x] = s;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int e = tid + x * TF_THREADS, m = e % 32, c = e / 32;
+        mpart[m * 33 + c] = tv[x];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int e = tid + x * TF_THREADS, rr = e % 32, c = e / 32;
+        double s = 0.0;
+        for (int m = rr; m < 32; ++m) s += ldg_cg(Tst + (size_t)(s0 + m) * ib + rr) * mpart[m * 33 + c];
+        Tst[(size_t)(cs + c) * ib + rr] = -s;  // T(rr, 32 + c)
+      }
+    }
+    __syncthreads();  // slab results (global) visible to the next slab's applies
+  }
+}
+
+}  // namespace tf

@@ -100,8 +100,9 @@ int main(int argc, char** argv) {
     cudaMemcpyToSymbol(g_probe, &pr, sizeof(pr));
     kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps);
     CK(cudaDeviceSynchronize());
-    printf("probe us/item: pre %.2f main %.2f epi %.2f\n", pr[0] / 1e3 / grid / reps, pr[1] / 1e3 / grid / reps,
-           pr[2] / 1e3 / grid / reps);
+    printf("probe us/item:");
+    for (int i = 0; i < 8; ++i) printf(" [%d] %.2f", i, pr[i] / 1e3 / grid / reps);
+    printf("\n");
   }
 #endif
   const double fl_task[] = {b * (double)b * b / 3, (double)b * b * b, (double)b * b * (b + 1.0), 2.0 * b * b * b,

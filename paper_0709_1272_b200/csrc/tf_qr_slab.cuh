@@ -229,16 +229,14 @@ __device__ inline void larfb_reg(const Ctx& cx, const double* VX, const double* 
 // sum; warp 0 then forms the Householder scalars, the top-row updates and the T column.
 template <int MI>
 __device__ inline void slab_panel(bool ts, double* P, int ldp, int cs, double* Rb, double* Ts, double* sm2) {
-  constexpr int CPT = 8 * MI, TPR = 32 / CPT;
+  constexpr int CPT = 8 * MI;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int u = lane / CPT, rr = lane % CPT, r = warp * CPT + rr, cb = u * CPT;
   double* part = sm2;          // 2 x 16 x 32 warp partials
-  double* sD = part + 1024;    // 32 column sums
-  double* sWc = sD + 32;       // 32: w_c
-  double* sH = sWc + 32;       // tau, den
-  (void)TPR;
-  for (int e = tid; e < 32 * 33; e += TF_THREADS) Ts[e] = 0.0;
-  __syncthreads();
+  double* sWc = part + 1024;   // 32: w_c
+  double* sH = sWc + 32;       // tau, 1/den
+  double* sS = sH + 2;         // 32 x 33: sdot_m of column jj (m < jj), for the T recurrence
+  double* sTau = sS + 32 * 33; // 32 taus
   for (int jj = 0; jj < 32; ++jj) {
     const int cg = cs + jj;
     const bool refl = ts || (r > cg);
@@ -258,51 +256,70 @@ __device__ inline void slab_panel(bool ts, double* P, int ldp, int cs, double* R
       }
     }
     double* pb = part + (jj & 1) * 512;
-    pb[warp * 32 + cb + rr] = v[0];
+    pb[warp * 32 + lane] = v[0];  // column cb + rr == lane
     __syncthreads();
     if (warp == 0) {
+      // Householder scalars of column jj (dlarfg without rescaling), then
+      // sdot_c = top_c + (column jj / den) . column c  (w_c for c > jj, V^T v for c < jj)
       const int c = lane;
-      double d = 0.0;
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll
-      for (int w = 0; w < TF_WARPS; ++w) d += pb[w * 32 + c];
+      for (int w = 0; w < TF_WARPS; w += 4) {
+        d0 += pb[w * 32 + c];
+        d1 += pb[(w + 1) * 32 + c];
+        d2 += pb[(w + 2) * 32 + c];
+        d3 += pb[(w + 3) * 32 + c];
+      }
+      const double d = (d0 + d1) + (d2 + d3);
       const double ss = __shfl_sync(0xffffffffu, d, jj);
       const double alpha = ts ? Rb[jj * 33 + jj] : P[cg + (size_t)jj * ldp];
-      const House h = make_house(alpha, ss);
-      // sdot_c = top_c + (column jj / den) . column c: w_c for c > jj, V^T v for c < jj
+      double tau = 0.0, beta = alpha, rden = 1.0;
+      if (ss != 0.0) {
+        const double nrm = sqrt(alpha * alpha + ss);
+        beta = (alpha >= 0.0) ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        rden = 1.0 / (alpha - beta);
+      }
       const double top = ts ? (c > jj ? Rb[jj * 33 + c] : 0.0) : (c != jj ? P[cg + (size_t)c * ldp] : 0.0);
-      const double sdot = top + d / h.den;
+      const double sdot = top + d * rden;
       if (c > jj) {
-        sWc[c] = sdot;
-        if (ts) Rb[jj * 33 + c] = top - h.tau * sdot;
-        else P[cg + (size_t)c * ldp] = top - h.tau * sdot;
+        sWc[c] = tau * sdot;
+        if (ts) Rb[jj * 33 + c] = top - tau * sdot;
+        else P[cg + (size_t)c * ldp] = top - tau * sdot;
       }
+      if (c < jj) sS[jj * 33 + c] = sdot;
       if (c == jj) {
-        if (ts) Rb[jj * 33 + jj] = h.beta;
-        else P[cg + (size_t)jj * ldp] = h.beta;
-        sH[0] = h.tau;
-        sH[1] = h.den;
+        if (ts) Rb[jj * 33 + jj] = beta;
+        else P[cg + (size_t)jj * ldp] = beta;
+        sH[0] = tau;
+        sH[1] = rden;
+        sTau[jj] = tau;
       }
-      // T column jj: T[m][jj] = sum_{m' < jj} T[m][m'] (-tau sdot_m'), T[jj][jj] = tau
-      double tcol = 0.0;
-      for (int mp = 0; mp < jj; ++mp) {
-        const double s_m = __shfl_sync(0xffffffffu, sdot, mp);
-        if (c < jj) tcol += Ts[c * 33 + mp] * (-h.tau * s_m);
-      }
-      if (c < jj) Ts[c * 33 + jj] = tcol;
-      if (c == jj) Ts[jj * 33 + jj] = h.tau;
     }
     __syncthreads();
-    const double tau = sH[0], den = sH[1];
     if (refl) {
-      const double vr = x / den;
+      const double vr = x * sH[1];
       if (jj >= cb && jj < cb + CPT) P[r + (size_t)jj * ldp] = vr;
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
         const int c = cb + k;
-        if (c > jj) P[r + (size_t)c * ldp] -= (tau * sWc[c]) * vr;
+        if (c > jj) P[r + (size_t)c * ldp] -= sWc[c] * vr;
       }
     }
     __syncwarp();
+  }
+  // T (32 x 32, upper; Ts[m*33 + c] = T(m, c)) by the column recurrence
+  // T(0:jj, jj) = -tau_jj T(0:jj, 0:jj) (V(:, 0:jj)^T v_jj), T(jj, jj) = tau_jj (warp 0)
+  if (warp == 0) {
+    const int c = lane;
+    for (int jj = 0; jj < 32; ++jj) {
+      const double tj = sTau[jj];
+      double acc = 0.0;
+      if (c < jj)
+        for (int m = c; m < jj; ++m) acc += Ts[c * 33 + m] * (-tj * sS[jj * 33 + m]);
+      Ts[c * 33 + jj] = c < jj ? acc : (c == jj ? tj : 0.0);
+      __syncwarp();
+    }
   }
   __syncthreads();
 }
@@ -319,6 +336,9 @@ __device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, dou
   const int ldp = b + 4;
   const double* Vsrc = ts ? A : VX;
   double acc[MI][SNJ][2];
+#ifdef TF_PROBE
+  unsigned long long t0 = probe_now();
+#endif
   for (int cs = 0; cs < b; cs += NSR) {
     const int t = cs / NSR;
     slab_load<MI>(acc, A + (size_t)cs * b, b);
@@ -333,9 +353,10 @@ __device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, dou
     double* P = sm;                              // b x 32, ld ldp
     double* Rb = P + 32 * ldp;                   // 32 x 33 (TSQRT)
     double* Ts = Rb + 32 * 33;                   // 32 x 33, Ts[m*33 + c] = T(m, c)
-    double* sm2 = Ts + 32 * 33;                  // panel scratch (1024 + 96)
-    double* mpart = sm2 + 1152;                  // 16 x 256 (T12 products)
+    double* sm2 = Ts + 32 * 33;                  // panel scratch (2146 doubles)
+    double* mpart = sm2;                         // 16 x 256 (T12 products; after the panel)
     double* sM = mpart + 4096;                   // 32 x 33
+    // smem: 32*ldp + 2*33*32 + 4096 + 33*32 doubles <= SMEM_USER for b <= 512
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -348,13 +369,20 @@ __device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, dou
         Rb[rr * 33 + c] = (rr <= c) ? ldg_cg(R + (cs + rr) + (size_t)(cs + c) * b) : 0.0;
       }
     __syncthreads();
+    TF_PROBE_MARK(0, t0);
     slab_panel<MI>(ts, P, ldp, cs, Rb, Ts, sm2);
+    TF_PROBE_MARK(1, t0);
     // ---- results: the slab, R block (TSQRT), V copy (GEQRT), T block(s)
-    for (int e = tid; e < b * 32; e += TF_THREADS) {
-      const int rr = e % b, c = e / b;
-      const double pv = P[rr + (size_t)c * ldp];
-      A[rr + (size_t)(cs + c) * b] = pv;
-      if (!ts) VX[rr + (size_t)(cs + c) * b] = rr > cs + c ? pv : (rr == cs + c ? 1.0 : 0.0);
+    {
+      constexpr int CPT = 8 * MI;  // the panel's thread layout: one row, CPT columns
+      const int u = lane / CPT, rw = warp * CPT + lane % CPT;
+#pragma unroll 4
+      for (int k = 0; k < CPT; ++k) {
+        const int c = u * CPT + k;
+        const double pv = P[rw + (size_t)c * ldp];
+        A[rw + (size_t)(cs + c) * b] = pv;
+        if (!ts) VX[rw + (size_t)(cs + c) * b] = rw > cs + c ? pv : (rw == cs + c ? 1.0 : 0.0);
+      }
     }
     if (ts)
       for (int e = tid; e < 32 * 32; e += TF_THREADS) {
@@ -426,6 +454,7 @@ __device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, dou
       }
     }
     __syncthreads();  // slab results (global) visible to the next slab's applies
+    TF_PROBE_MARK(2, t0);
   }
 }
 

@@ -699,8 +699,8 @@ __device__ inline int getrf_item(const Ctx& cx, double* A, int* ipiv, double* LX
   return first_zero;
 }
 
-// GESSM: slab `item` of A_kj <- L_kk^{-1} P_kk A_kj.
-__device__ inline void gessm_item(const Ctx& cx, const double* LX, const int* ipiv, double* C, int item,
+// GESSM reference-blocked path: slab `item` of A_kj <- L_kk^{-1} P_kk A_kj.
+__device__ inline void gessm_ref(const Ctx& cx, const double* LX, const int* ipiv, double* C, int item,
                                   double* sm) {
   const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
   const int n0 = item * NS, nc = min(NS, b - n0);
@@ -840,8 +840,8 @@ __device__ inline int tstrf_item(const Ctx& cx, double* U, double* A, double* Ls
   return first_zero;
 }
 
-// SSSSM: slab `item` of [U; A] <- L_ik^{-1} P_ik [U; A].
-__device__ inline void ssssm_item(const Ctx& cx, const double* L, const double* Ls, const int* ipiv, double* U,
+// SSSSM reference-blocked path: slab `item` of [U; A] <- L_ik^{-1} P_ik [U; A].
+__device__ inline void ssssm_ref(const Ctx& cx, const double* L, const double* Ls, const int* ipiv, double* U,
                                   double* A, int item, double* sm) {
   const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
   const int n0 = item * NS, nc = min(NS, b - n0);
@@ -862,6 +862,22 @@ __device__ inline void ssssm_item(const Ctx& cx, const double* L, const double* 
     update_mn(sm, A, b, L + (size_t)c0 * b, b, U + c0, b, b, nc, ib);
     __syncthreads();
   }
+}
+
+}  // namespace tf
+#include "tf_lu_slab.cuh"
+namespace tf {
+
+// LU update task kernels: register-slab path for b in {128, 256, 512}, ib in {32, 64}.
+__device__ inline void gessm_item(const Ctx& cx, const double* LX, const int* ipiv, double* C, int item,
+                                  double* sm) {
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(gessm_reg, cx, LX, ipiv, C, item, sm);
+  else gessm_ref(cx, LX, ipiv, C, item, sm);
+}
+__device__ inline void ssssm_item(const Ctx& cx, const double* L, const double* Ls, const int* ipiv, double* U,
+                                  double* A, int item, double* sm) {
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(ssssm_reg, cx, L, Ls, ipiv, U, A, item, sm);
+  else ssssm_ref(cx, L, Ls, ipiv, U, A, item, sm);
 }
 
 }  // namespace tf

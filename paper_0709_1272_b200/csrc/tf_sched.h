@@ -33,8 +33,8 @@ constexpr int K_SEND = 12, K_RECV = 13;
 
 TF_HD inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
-// QR register-slab kernels (tf_qr_slab.cuh: SSRFB / LARFB items of NSR columns, slab-wise
-// GEQRT / TSQRT): b in {128, 256, 512}, ib in {32, 64}.
+// Register-slab kernels (tf_qr_slab.cuh: SSRFB / LARFB items of NSR columns, slab-wise
+// GEQRT / TSQRT; tf_lu_slab.cuh: GESSM / SSSSM items): b in {128, 256, 512}, ib in {32, 64}.
 constexpr int NSR = 32;
 TF_HD inline bool ssrfb_reg_ok(int b, int ib) { return b % 128 == 0 && b <= 512 && ib % 32 == 0 && ib <= 64; }
 
@@ -44,8 +44,7 @@ TF_HD inline int items_of(int kind, int b, int ib) {
     case 1: return nr;                 // TRSM: row blocks
     case 2: return nr * (nr + 1) / 2;  // SYRK: lower sub-tiles
     case 3: return nr * nr;            // GEMM: sub-tiles
-    case 5: case 7: return ssrfb_reg_ok(b, ib) ? b / NSR : ceil_div(b, NS);
-    case 9: case 11: return ceil_div(b, NS);  // slabs
+    case 5: case 7: case 9: case 11: return ssrfb_reg_ok(b, ib) ? b / NSR : ceil_div(b, NS);  // slabs
     default: return 1;                 // panels, RECV
   }
 }

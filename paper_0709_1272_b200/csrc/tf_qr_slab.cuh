@@ -217,106 +217,148 @@ __device__ inline void larfb_reg(const Ctx& cx, const double* VX, const double* 
   slab_store<MI>(acc, C, b);
 }
 
-// Householder factorization of one 32-column slab held in shared memory (P, b x 32,
+// Householder factorization of one 32-column slab (P in smem on entry and exit: b x 32,
 // column-major, ld ldp), column by column (PAPER.md:362-372 / 390-404).
 //   ts   : TSQRT — reflector rows are all b rows of P, the top element of each reflector
 //          is the diagonal of Rb (32 x 32, ld 33, upper part = R rows/cols of the slab),
 //          whose rows receive the top components of the updates.
 //   !ts  : GEQRT — column jj's reflector covers rows > cs + jj of P; row cs + jj is the top.
-// Thread layout: TPR = 4/MI threads per row, each owning CPT = 8*MI contiguous columns;
-// lane = u*CPT + rr (row w*CPT + rr, columns [u*CPT, (u+1)*CPT)).  Per column: the dots of
-// column jj with all 32 columns (the norm included) in one reduce-scatter + cross-warp
-// sum; warp 0 then forms the Householder scalars, the top-row updates and the T column.
-template <int MI>
-__device__ inline void slab_panel(bool ts, double* P, int ldp, int cs, double* Rb, double* Ts, double* sm2) {
-  constexpr int CPT = 8 * MI;
+// Layout during the factorization: warp w keeps rows [w*RW, (w+1)*RW) (RW = b/16) and lane c
+// keeps column c of them in registers.  Per column jj: every lane forms the dot of its
+// column with column jj over the warp's rows (column jj's entries come from lane jj by
+// shuffles), the 16 warp partials go through shared memory, and after ONE CTA barrier every
+// warp sums them in the same fixed order, forms the Householder scalars itself (bitwise
+// identical in all warps) and applies the rank-1 update to its rows.  Double-buffered
+// partials / top rows make the single barrier per column sufficient.
+template <int MI, bool TS>
+__device__ inline void slab_panel(double* P, int ldp, int cs, double* Rb, double* Ts, double* sm2) {
+  constexpr int RW = 8 * MI;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int u = lane / CPT, rr = lane % CPT, r = warp * CPT + rr, cb = u * CPT;
+  const int c = lane, r0w = warp * RW;
   double* part = sm2;          // 2 x 16 x 32 warp partials
-  double* sWc = part + 1024;   // 32: w_c
-  double* sH = sWc + 32;       // tau, 1/den
-  double* sS = sH + 2;         // 32 x 33: sdot_m of column jj (m < jj), for the T recurrence
+  double* sS = part + 1024;    // 32 x 33: sdot_m of column jj (m < jj), for the T recurrence
   double* sTau = sS + 32 * 33; // 32 taus
+  double* sTop = sTau + 32;    // GEQRT: 2 x 32 top rows (by column parity)
+  double* Rbn = sTop + 64;     // TSQRT: 32 x 33 finished R rows (Rb stays read-only)
+  double* xcol = Rbn + 32 * 33;  // 16 x RW: column jj of each warp's rows (16-byte aligned)
+  double* xw = xcol + warp * RW;
+  double p[RW];
+#pragma unroll
+  for (int k = 0; k < RW; ++k) p[k] = P[(r0w + k) + (size_t)c * ldp];
   for (int jj = 0; jj < 32; ++jj) {
     const int cg = cs + jj;
-    const bool refl = ts || (r > cg);
-    const double x = refl ? P[r + (size_t)jj * ldp] : 0.0;
-    double v[CPT];
+    const int kcg = cg - r0w;  // the top row's index in this warp (GEQRT)
+    // warp classes (GEQRT): all rows below the top row (no masks), the warp holding the top
+    // row (masks), all rows at or above it (no work); TSQRT: every row is a reflector row
+    const bool full = TS || kcg < 0;
+    const bool none = !TS && kcg >= RW;
+    // column jj of this warp's rows, broadcast through shared memory
+    __syncwarp();
+    if (c == jj && !none)
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) v[k] = x * P[r + (size_t)(cb + k) * ldp];
-    // reduce-scatter over the CPT lanes of this column group: lane keeps column cb + rr
+      for (int k = 0; k < RW; ++k) xw[k] = p[k];
+    __syncwarp();
+    double d0 = 0.0, d1 = 0.0;
+    if (full) {
 #pragma unroll
-    for (int m = CPT / 2, n = CPT; m >= 1; m >>= 1, n >>= 1) {
-      const bool up = lane & m;
-#pragma unroll
-      for (int k = 0; k < n / 2; ++k) {
-        const double send = up ? v[k] : v[k + n / 2];
-        const double keep = up ? v[k + n / 2] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      for (int k = 0; k < RW; k += 2) {
+        const double2 x2 = *reinterpret_cast<const double2*>(xw + k);
+        d0 = fma(x2.x, p[k], d0);
+        d1 = fma(x2.y, p[k + 1], d1);
       }
+    } else if (!none) {
+#pragma unroll
+      for (int k = 0; k < RW; k += 2) {
+        const double2 x2 = *reinterpret_cast<const double2*>(xw + k);
+        if (k > kcg) d0 = fma(x2.x, p[k], d0);
+        if (k + 1 > kcg) d1 = fma(x2.y, p[k + 1], d1);
+      }
+    }
+    double* top_row = sTop + (jj & 1) * 32;
+    if (!TS && kcg >= 0 && kcg < RW) {  // publish the top row
+      double tv = 0.0;
+#pragma unroll
+      for (int k = 0; k < RW; ++k)
+        if (k == kcg) tv = p[k];
+      top_row[c] = tv;
     }
     double* pb = part + (jj & 1) * 512;
-    pb[warp * 32 + lane] = v[0];  // column cb + rr == lane
+    pb[warp * 32 + c] = d0 + d1;
     __syncthreads();
+    // every warp: column sums (fixed order), Householder scalars, w_c of its lane's column
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+#pragma unroll
+    for (int w = 0; w < TF_WARPS; w += 4) {
+      e0 += pb[w * 32 + c];
+      e1 += pb[(w + 1) * 32 + c];
+      e2 += pb[(w + 2) * 32 + c];
+      e3 += pb[(w + 3) * 32 + c];
+    }
+    const double dd = (e0 + e1) + (e2 + e3);
+    const double ss = __shfl_sync(0xffffffffu, dd, jj);
+    const double alpha = TS ? Rb[jj * 33 + jj] : top_row[jj];
+    double tau = 0.0, beta = alpha, rden = 1.0;
+    if (ss != 0.0) {
+      const double nrm = sqrt(alpha * alpha + ss);
+      beta = (alpha >= 0.0) ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      rden = 1.0 / (alpha - beta);
+    }
+    const double top = TS ? (c > jj ? Rb[jj * 33 + c] : 0.0) : (c != jj ? top_row[c] : 0.0);
+    const double sdot = top + dd * rden;
+    const double tw = c > jj ? tau * sdot : 0.0;
     if (warp == 0) {
-      // Householder scalars of column jj (dlarfg without rescaling), then
-      // sdot_c = top_c + (column jj / den) . column c  (w_c for c > jj, V^T v for c < jj)
-      const int c = lane;
-      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-#pragma unroll
-      for (int w = 0; w < TF_WARPS; w += 4) {
-        d0 += pb[w * 32 + c];
-        d1 += pb[(w + 1) * 32 + c];
-        d2 += pb[(w + 2) * 32 + c];
-        d3 += pb[(w + 3) * 32 + c];
-      }
-      const double d = (d0 + d1) + (d2 + d3);
-      const double ss = __shfl_sync(0xffffffffu, d, jj);
-      const double alpha = ts ? Rb[jj * 33 + jj] : P[cg + (size_t)jj * ldp];
-      double tau = 0.0, beta = alpha, rden = 1.0;
-      if (ss != 0.0) {
-        const double nrm = sqrt(alpha * alpha + ss);
-        beta = (alpha >= 0.0) ? -nrm : nrm;
-        tau = (beta - alpha) / beta;
-        rden = 1.0 / (alpha - beta);
-      }
-      const double top = ts ? (c > jj ? Rb[jj * 33 + c] : 0.0) : (c != jj ? P[cg + (size_t)c * ldp] : 0.0);
-      const double sdot = top + d * rden;
-      if (c > jj) {
-        sWc[c] = tau * sdot;
-        if (ts) Rb[jj * 33 + c] = top - tau * sdot;
-        else P[cg + (size_t)c * ldp] = top - tau * sdot;
-      }
+      if (TS && c > jj) Rbn[jj * 33 + c] = top - tw;
+      if (TS && c == jj) Rbn[jj * 33 + jj] = beta;
       if (c < jj) sS[jj * 33 + c] = sdot;
-      if (c == jj) {
-        if (ts) Rb[jj * 33 + jj] = beta;
-        else P[cg + (size_t)jj * ldp] = beta;
-        sH[0] = tau;
-        sH[1] = rden;
-        sTau[jj] = tau;
-      }
+      if (c == jj) sTau[jj] = tau;
     }
-    __syncthreads();
-    if (refl) {
-      const double vr = x * sH[1];
-      if (jj >= cb && jj < cb + CPT) P[r + (size_t)jj * ldp] = vr;
+    // rank-1 update: p <- fac*p - tw*(x*rden); lane jj (tw = 0, fac = rden) becomes v
+    const double fac = (c == jj) ? rden : 1.0;
+    if (full) {
 #pragma unroll
-      for (int k = 0; k < CPT; ++k) {
-        const int c = cb + k;
-        if (c > jj) P[r + (size_t)c * ldp] -= sWc[c] * vr;
+      for (int k = 0; k < RW; k += 2) {
+        const double2 x2 = *reinterpret_cast<const double2*>(xw + k);
+        p[k] = fma(-tw, x2.x * rden, p[k] * fac);
+        p[k + 1] = fma(-tw, x2.y * rden, p[k + 1] * fac);
+      }
+    } else if (!none) {
+#pragma unroll
+      for (int k = 0; k < RW; k += 2) {
+        const double2 x2 = *reinterpret_cast<const double2*>(xw + k);
+        if (k > kcg) p[k] = fma(-tw, x2.x * rden, p[k] * fac);
+        if (k + 1 > kcg) p[k + 1] = fma(-tw, x2.y * rden, p[k + 1] * fac);
+      }
+      if (kcg >= 0) {  // GEQRT top row: R entries of row cg
+#pragma unroll
+        for (int k = 0; k < RW; ++k)
+          if (k == kcg) p[k] = (c == jj) ? beta : p[k] - tw;
       }
     }
-    __syncwarp();
   }
-  // T (32 x 32, upper; Ts[m*33 + c] = T(m, c)) by the column recurrence
-  // T(0:jj, jj) = -tau_jj T(0:jj, 0:jj) (V(:, 0:jj)^T v_jj), T(jj, jj) = tau_jj (warp 0)
+#pragma unroll
+  for (int k = 0; k < RW; ++k) P[(r0w + k) + (size_t)c * ldp] = p[k];
+  __syncthreads();
+  if (TS)  // finished R rows (upper triangle incl. the diagonal)
+    for (int e = tid; e < 32 * 32; e += TF_THREADS) {
+      const int rr = e / 32, cc = e % 32;
+      if (rr <= cc) Rb[rr * 33 + cc] = Rbn[rr * 33 + cc];
+    }
+  // T (32 x 32, upper; Ts[m*33 + c] = T(m, c)) by the column recurrence (warp 0)
+  // (uniform trip counts with T(c, m) = 0 for m < c, four independent partial sums)
   if (warp == 0) {
-    const int c = lane;
     for (int jj = 0; jj < 32; ++jj) {
       const double tj = sTau[jj];
-      double acc = 0.0;
-      if (c < jj)
-        for (int m = c; m < jj; ++m) acc += Ts[c * 33 + m] * (-tj * sS[jj * 33 + m]);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int m = 0;
+      for (; m + 3 < jj; m += 4) {
+        a0 += Ts[c * 33 + m] * sS[jj * 33 + m];
+        a1 += Ts[c * 33 + m + 1] * sS[jj * 33 + m + 1];
+        a2 += Ts[c * 33 + m + 2] * sS[jj * 33 + m + 2];
+        a3 += Ts[c * 33 + m + 3] * sS[jj * 33 + m + 3];
+      }
+      for (; m < jj; ++m) a0 += Ts[c * 33 + m] * sS[jj * 33 + m];
+      const double acc = -tj * ((a0 + a1) + (a2 + a3));
       Ts[c * 33 + jj] = c < jj ? acc : (c == jj ? tj : 0.0);
       __syncwarp();
     }
@@ -333,7 +375,7 @@ __device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, dou
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   constexpr int RW = 8 * MI;
   const int r0 = warp * RW;
-  const int ldp = b + 4;
+  const int ldp = b + 1;  // odd: the panel's per-lane column loads hit distinct banks
   const double* Vsrc = ts ? A : VX;
   double acc[MI][SNJ][2];
 #ifdef TF_PROBE
@@ -353,7 +395,7 @@ __device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, dou
     double* P = sm;                              // b x 32, ld ldp
     double* Rb = P + 32 * ldp;                   // 32 x 33 (TSQRT)
     double* Ts = Rb + 32 * 33;                   // 32 x 33, Ts[m*33 + c] = T(m, c)
-    double* sm2 = Ts + 32 * 33;                  // panel scratch (2146 doubles)
+    double* sm2 = Ts + 32 * 33;                  // panel scratch (3232 + 16*RW doubles)
     double* mpart = sm2;                         // 16 x 256 (T12 products; after the panel)
     double* sM = mpart + 4096;                   // 32 x 33
     // smem: 32*ldp + 2*33*32 + 4096 + 33*32 doubles <= SMEM_USER for b <= 512
@@ -370,7 +412,8 @@ __device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, dou
       }
     __syncthreads();
     TF_PROBE_MARK(0, t0);
-    slab_panel<MI>(ts, P, ldp, cs, Rb, Ts, sm2);
+    if (ts) slab_panel<MI, true>(P, ldp, cs, Rb, Ts, sm2);
+    else slab_panel<MI, false>(P, ldp, cs, Rb, Ts, sm2);
     TF_PROBE_MARK(1, t0);
     // ---- results: the slab, R block (TSQRT), V copy (GEQRT), T block(s)
     {

@@ -640,7 +640,7 @@ __device__ inline int build_slots(const int* ipiv, int c0, int ib, int b, int* j
 // GETRF: LAPACK dgetrf semantics with block ib, whole-tile-row swaps
 // (Z12), first-max pivot (Z11).  Writes LX (explicit unit-lower copy of L_kk) for the
 // GESSM items.  Returns the first zero-pivot local column or -1.
-__device__ inline int getrf_item(const Ctx& cx, double* A, int* ipiv, double* LX, double* sm) {
+__device__ inline int getrf_ref(const Ctx& cx, double* A, int* ipiv, double* LX, double* sm) {
   const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
   double* redv = sm;
   int* redi = reinterpret_cast<int*>(redv + TF_WARPS);
@@ -788,7 +788,7 @@ __device__ inline int tstrf_panel(double* P, int ldp, int b, double* Ub, double*
 }
 
 // TSTRF: pairwise-pivoted LU of [U; A] (upper region of U only).
-__device__ inline int tstrf_item(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, double* sm) {
+__device__ inline int tstrf_ref(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, double* sm) {
   const int b = cx.b, ib = cx.ib, tid = threadIdx.x;
   int first_zero = -1;
   for (int c0 = 0; c0 < b; c0 += ib) {
@@ -878,6 +878,16 @@ __device__ inline void ssssm_item(const Ctx& cx, const double* L, const double* 
                                   double* A, int item, double* sm) {
   if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(ssssm_reg, cx, L, Ls, ipiv, U, A, item, sm);
   else ssssm_ref(cx, L, Ls, ipiv, U, A, item, sm);
+}
+// LU panel tasks: slab kernels for ib = 32 (the slab is the inner block).
+#define TF_SLAB_RET(fn, ...) (cx.b == 512 ? fn<4>(__VA_ARGS__) : cx.b == 256 ? fn<2>(__VA_ARGS__) : fn<1>(__VA_ARGS__))
+__device__ inline int getrf_item(const Ctx& cx, double* A, int* ipiv, double* LX, double* sm) {
+  if (ssrfb_reg_ok(cx.b, cx.ib) && cx.ib == 32) return TF_SLAB_RET(getrf_slab, cx, A, ipiv, LX, sm);
+  return getrf_ref(cx, A, ipiv, LX, sm);
+}
+__device__ inline int tstrf_item(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, double* sm) {
+  if (ssrfb_reg_ok(cx.b, cx.ib) && cx.ib == 32) return TF_SLAB_RET(tstrf_slab, cx, U, A, Ls, ipiv, sm);
+  return tstrf_ref(cx, U, A, Ls, ipiv, sm);
 }
 
 }  // namespace tf

@@ -32,115 +32,118 @@ __device__ __forceinline__ void lu_block_solve(double* sU, const double* sL, int
   __syncwarp();
 }
 
-// SSSSM item: 32 columns of [U_kj; A_ij].  L = A_ik (multipliers), Ls = L strip (i,k),
-// ipiv = pivots (i,k) in [1, 2b] (b + r + 1 = bottom row r swapped in, SURVEY Z13).
+// One inner block of the pairwise-pivoted update on a register slab (SSSSM step):
+// [U_s; A] <- swaps of block s, U_s <- (I + Ls_s)^{-1} U_s, A -= L[:, s] U_s.
+//   Us  : U rows c0.. of the slab columns, (m, c) at Us[m + c*b] (read, then written back)
+//   Lc  : L columns of the block, (r, m) at Lc[r + m*b]
+//   Lsb : Ls block s, (r, m) at Lsb[r + m*ib];  pv: the block's ib pivots (1-based, [1, 2b])
 template <int MI>
-__device__ inline void ssssm_reg(const Ctx& cx, const double* L, const double* Ls, const int* ipiv, double* U,
-                                 double* A, int item, double* sm) {
+__device__ __forceinline__ void lu_ts_apply(double (&acc)[MI][SNJ][2], double* Us, const double* Lc, const double* Lsb,
+                                            const int* pv, int ib, int b, double* sm) {
   constexpr int RW = 8 * MI;
-  const int b = cx.b, ib = cx.ib;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   const int r0 = warp * RW;
-  U += (size_t)item * NSR * b;
-  A += (size_t)item * NSR * b;
   double* sU = sm;                              // ib x LU_LDW: U_s
   double* sA = sU + 64 * LU_LDW;                // ib slots x LU_LDW: the A rows the pivots name
   double* sL = sA + 64 * LU_LDW;                // ib x (ib+1): L(r, m), r > m
   int* flag = reinterpret_cast<int*>(sL + 64 * 65);  // b: slot of bottom row r (INT_MAX = none)
   int* spv = flag + 512;                        // ib pivots of the block
+  for (int r = tid; r < b; r += TF_THREADS) flag[r] = INT_MAX;
+  for (int e = tid; e < ib * NSR; e += TF_THREADS) {
+    const int m = e % ib, c = e / ib;
+    sU[m * LU_LDW + c] = ldg_cg(Us + m + (size_t)c * b);
+  }
+  for (int e = tid; e < ib * ib; e += TF_THREADS) {
+    const int r = e % ib, m = e / ib;
+    sL[r * (ib + 1) + m] = (r > m) ? ldg_cg(Lsb + e) : 0.0;
+  }
+  __syncthreads();
+  if (tid < ib) {
+    const int v = pv[tid];
+    spv[tid] = v;
+    if (v > b) atomicMin(&flag[v - b - 1], tid);  // slot = first pivot naming the row
+  }
+  __syncthreads();
+  // named A rows: registers -> smem slots
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int f = flag[r0 + 8 * i + g];
+    if (f != INT_MAX)
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) sA[f * LU_LDW + 8 * j + 2 * q + e] = acc[i][j][e];
+  }
+  __syncthreads();
+  // pairwise swaps in pivot order, then the unit-lower solve (per column)
+  {
+    const int c = tid >> 4;
+    if ((tid & 15) == 0)
+      for (int jj = 0; jj < ib; ++jj) {
+        const int v = spv[jj];
+        if (v > b) {
+          const int f = flag[v - b - 1];
+          const double t = sU[jj * LU_LDW + c];
+          sU[jj * LU_LDW + c] = sA[f * LU_LDW + c];
+          sA[f * LU_LDW + c] = t;
+        }
+      }
+    lu_block_solve(sU, sL, ib);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < MI; ++i) {
+    const int f = flag[r0 + 8 * i + g];
+    if (f != INT_MAX)
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) acc[i][j][e] = sA[f * LU_LDW + 8 * j + 2 * q + e];
+  }
+  for (int e = tid; e < ib * NSR; e += TF_THREADS) {
+    const int m = e % ib, c = e / ib;
+    Us[m + (size_t)c * b] = sU[m * LU_LDW + c];
+  }
+  // A -= L[:, block] U_s
+  for (int ks = 0; ks < ib / 4; ++ks) {
+    double a[MI], bq[SNJ];
+#pragma unroll
+    for (int i = 0; i < MI; ++i) a[i] = -Lc[(r0 + 8 * i + g) + (size_t)(4 * ks + q) * b];
+#pragma unroll
+    for (int j = 0; j < SNJ; ++j) bq[j] = sU[(4 * ks + q) * LU_LDW + 8 * j + g];
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j) dmma(acc[i][j], a[i], bq[j]);
+  }
+  __syncthreads();
+}
+
+// SSSSM item: 32 columns of [U_kj; A_ij].  L = A_ik (multipliers), Ls = L strip (i,k),
+// ipiv = pivots (i,k) in [1, 2b] (b + r + 1 = bottom row r swapped in, SURVEY Z13).
+template <int MI>
+__device__ inline void ssssm_reg(const Ctx& cx, const double* L, const double* Ls, const int* ipiv, double* U,
+                                 double* A, int item, double* sm) {
+  const int b = cx.b, ib = cx.ib;
+  U += (size_t)item * NSR * b;
+  A += (size_t)item * NSR * b;
   double acc[MI][SNJ][2];
   slab_load<MI>(acc, A, b);
-  for (int c0 = 0; c0 < b; c0 += ib) {
-    for (int r = tid; r < b; r += TF_THREADS) flag[r] = INT_MAX;
-    for (int e = tid; e < ib * NSR; e += TF_THREADS) {
-      const int m = e % ib, c = e / ib;
-      sU[m * LU_LDW + c] = ldg_cg(U + (c0 + m) + (size_t)c * b);
-    }
-    for (int e = tid; e < ib * ib; e += TF_THREADS) {
-      const int r = e % ib, m = e / ib;
-      sL[r * (ib + 1) + m] = (r > m) ? ldg_cg(Ls + (size_t)c0 * ib + e) : 0.0;
-    }
-    __syncthreads();
-    if (tid < ib) {
-      const int pv = ipiv[c0 + tid];
-      spv[tid] = pv;
-      if (pv > b) atomicMin(&flag[pv - b - 1], tid);  // slot = first pivot naming the row
-    }
-    __syncthreads();
-    // named A rows: registers -> smem slots
-#pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int f = flag[r0 + 8 * i + g];
-      if (f != INT_MAX)
-#pragma unroll
-        for (int j = 0; j < SNJ; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) sA[f * LU_LDW + 8 * j + 2 * q + e] = acc[i][j][e];
-    }
-    __syncthreads();
-    // pairwise swaps in pivot order, then the unit-lower solve (per column)
-    {
-      const int c = tid >> 4;
-      if ((tid & 15) == 0)
-        for (int jj = 0; jj < ib; ++jj) {
-          const int pv = spv[jj];
-          if (pv > b) {
-            const int f = flag[pv - b - 1];
-            const double t = sU[jj * LU_LDW + c];
-            sU[jj * LU_LDW + c] = sA[f * LU_LDW + c];
-            sA[f * LU_LDW + c] = t;
-          }
-        }
-      lu_block_solve(sU, sL, ib);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int f = flag[r0 + 8 * i + g];
-      if (f != INT_MAX)
-#pragma unroll
-        for (int j = 0; j < SNJ; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) acc[i][j][e] = sA[f * LU_LDW + 8 * j + 2 * q + e];
-    }
-    for (int e = tid; e < ib * NSR; e += TF_THREADS) {
-      const int m = e % ib, c = e / ib;
-      U[(c0 + m) + (size_t)c * b] = sU[m * LU_LDW + c];
-    }
-    // A -= L[:, c0:c0+ib] U_s
-    for (int ks = 0; ks < ib / 4; ++ks) {
-      double a[MI], bq[SNJ];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) a[i] = -L[(r0 + 8 * i + g) + (size_t)(c0 + 4 * ks + q) * b];
-#pragma unroll
-      for (int j = 0; j < SNJ; ++j) bq[j] = sU[(4 * ks + q) * LU_LDW + 8 * j + g];
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < SNJ; ++j) dmma(acc[i][j], a[i], bq[j]);
-    }
-    __syncthreads();
-  }
+  for (int c0 = 0; c0 < b; c0 += ib)
+    lu_ts_apply<MI>(acc, U + c0, L + (size_t)c0 * b, Ls + (size_t)c0 * ib, ipiv + c0, ib, b, sm);
   slab_store<MI>(acc, A, b);
 }
 
-// GESSM item: 32 columns of C = A_kj <- L_kk^{-1} P_kk C.  LX = explicit unit-lower L_kk
-// copy (b x b), ipiv = GETRF interchanges in [1, b] (LAPACK form, Z12).
+// Row interchanges j <-> ipiv[j]-1, j = j0..j1-1 in order (LAPACK form), applied to the
+// register slab: composed into a gather permutation, applied through shared memory.
 template <int MI>
-__device__ inline void gessm_reg(const Ctx& cx, const double* LX, const int* ipiv, double* C, int item,
-                                 double* sm) {
+__device__ __forceinline__ void lu_rows_permute(double (&acc)[MI][SNJ][2], const int* ipiv, int j0, int j1, int b,
+                                                double* sm) {
   constexpr int RW = 8 * MI;
-  const int b = cx.b, ib = cx.ib;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   const int r0 = warp * RW;
-  C += (size_t)item * NSR * b;
-  double* sC = sm;                              // b x LU_LDW (permutation staging)
-  double* sU = sm;                              // ib x LU_LDW (after the permutation)
-  double* sL = sU + 64 * LU_LDW;                // ib x (ib+1)
-  int* perm = reinterpret_cast<int*>(sm + 512 * LU_LDW);
-  double acc[MI][SNJ][2];
-  slab_load<MI>(acc, C, b);
-  // P_kk: compose the b sequential interchanges into a gather permutation
+  double* sC = sm;                                        // b x LU_LDW
+  int* perm = reinterpret_cast<int*>(sm + 512 * LU_LDW);  // b
   for (int r = tid; r < b; r += TF_THREADS) perm[r] = r;
 #pragma unroll
   for (int i = 0; i < MI; ++i)
@@ -150,7 +153,7 @@ __device__ inline void gessm_reg(const Ctx& cx, const double* LX, const int* ipi
       for (int e = 0; e < 2; ++e) sC[(r0 + 8 * i + g) * LU_LDW + 8 * j + 2 * q + e] = acc[i][j][e];
   __syncthreads();
   if (tid == 0)
-    for (int j = 0; j < b; ++j) {
+    for (int j = j0; j < j1; ++j) {
       const int r = ipiv[j] - 1;
       const int t = perm[j];
       perm[j] = perm[r];
@@ -166,55 +169,299 @@ __device__ inline void gessm_reg(const Ctx& cx, const double* LX, const int* ipi
       for (int e = 0; e < 2; ++e) acc[i][j][e] = sC[src * LU_LDW + 8 * j + 2 * q + e];
   }
   __syncthreads();
-  // blocked unit-lower forward solve
-  for (int c0 = 0; c0 < b; c0 += ib) {
-    const int c1 = c0 + ib;
-    // block rows -> smem (their owner warps), L block
+}
+
+// Block [c0, c0+ib) of the unit-lower solve on the register slab: its rows <- L_ss^{-1} rows
+// (forward substitution), rows below -= L[rows, c0:c0+ib] * block rows (DMMA).  Lt: the tile
+// holding L (explicit unit-lower copy or the factored tile itself; only r > c is read).
+template <int MI>
+__device__ __forceinline__ void lu_rows_block(double (&acc)[MI][SNJ][2], const double* Lt, int c0, int ib, int b,
+                                              double* sm) {
+  constexpr int RW = 8 * MI;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+  const int r0 = warp * RW;
+  const int c1 = c0 + ib;
+  double* sU = sm;                // ib x LU_LDW
+  double* sL = sU + 64 * LU_LDW;  // ib x (ib+1)
 #pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int row = r0 + 8 * i + g;
-      if (row >= c0 && row < c1)
+  for (int i = 0; i < MI; ++i) {
+    const int row = r0 + 8 * i + g;
+    if (row >= c0 && row < c1)
 #pragma unroll
-        for (int j = 0; j < SNJ; ++j)
+      for (int j = 0; j < SNJ; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) sU[(row - c0) * LU_LDW + 8 * j + 2 * q + e] = acc[i][j][e];
-    }
-    for (int e = tid; e < ib * ib; e += TF_THREADS) {
-      const int r = e % ib, m = e / ib;
-      sL[r * (ib + 1) + m] = (r > m) ? ldg_cg(LX + (c0 + r) + (size_t)(c0 + m) * b) : 0.0;
-    }
-    __syncthreads();
-    lu_block_solve(sU, sL, ib);
-    __syncthreads();
+        for (int e = 0; e < 2; ++e) sU[(row - c0) * LU_LDW + 8 * j + 2 * q + e] = acc[i][j][e];
+  }
+  for (int e = tid; e < ib * ib; e += TF_THREADS) {
+    const int r = e % ib, m = e / ib;
+    sL[r * (ib + 1) + m] = (r > m) ? ldg_cg(Lt + (c0 + r) + (size_t)(c0 + m) * b) : 0.0;
+  }
+  __syncthreads();
+  lu_block_solve(sU, sL, ib);
+  __syncthreads();
 #pragma unroll
-    for (int i = 0; i < MI; ++i) {
-      const int row = r0 + 8 * i + g;
-      if (row >= c0 && row < c1)
+  for (int i = 0; i < MI; ++i) {
+    const int row = r0 + 8 * i + g;
+    if (row >= c0 && row < c1)
 #pragma unroll
-        for (int j = 0; j < SNJ; ++j)
+      for (int j = 0; j < SNJ; ++j)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) acc[i][j][e] = sU[(row - c0) * LU_LDW + 8 * j + 2 * q + e];
-    }
-    // rows below the block: C -= L[:, c0:c1] C_s
-    if (c1 < b && r0 + RW > c1) {
-      for (int ks = 0; ks < ib / 4; ++ks) {
-        double a[MI], bq[SNJ];
+        for (int e = 0; e < 2; ++e) acc[i][j][e] = sU[(row - c0) * LU_LDW + 8 * j + 2 * q + e];
+  }
+  if (c1 < b && r0 + RW > c1) {
+    for (int ks = 0; ks < ib / 4; ++ks) {
+      double a[MI], bq[SNJ];
 #pragma unroll
-        for (int i = 0; i < MI; ++i) {
-          const int row = r0 + 8 * i + g;
-          a[i] = row >= c1 ? -LX[row + (size_t)(c0 + 4 * ks + q) * b] : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < SNJ; ++j) bq[j] = sU[(4 * ks + q) * LU_LDW + 8 * j + g];
-#pragma unroll
-        for (int i = 0; i < MI; ++i)
-#pragma unroll
-          for (int j = 0; j < SNJ; ++j) dmma(acc[i][j], a[i], bq[j]);
+      for (int i = 0; i < MI; ++i) {
+        const int row = r0 + 8 * i + g;
+        a[i] = row >= c1 ? -Lt[row + (size_t)(c0 + 4 * ks + q) * b] : 0.0;
       }
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j) bq[j] = sU[(4 * ks + q) * LU_LDW + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < SNJ; ++j) dmma(acc[i][j], a[i], bq[j]);
+    }
+  }
+  __syncthreads();
+}
+
+// GESSM item: 32 columns of C = A_kj <- L_kk^{-1} P_kk C.  LX = explicit unit-lower L_kk
+// copy (b x b), ipiv = GETRF interchanges in [1, b] (LAPACK form, Z12).
+template <int MI>
+__device__ inline void gessm_reg(const Ctx& cx, const double* LX, const int* ipiv, double* C, int item,
+                                 double* sm) {
+  const int b = cx.b, ib = cx.ib;
+  C += (size_t)item * NSR * b;
+  double acc[MI][SNJ][2];
+  slab_load<MI>(acc, C, b);
+  lu_rows_permute<MI>(acc, ipiv, 0, b, b, sm);
+  for (int c0 = 0; c0 < b; c0 += ib) lu_rows_block<MI>(acc, LX, c0, ib, b, sm);
+  slab_store<MI>(acc, C, b);
+}
+
+// LU panel of one 32-column slab held as P (smem, b x 32, column-major, ld ldp) on entry and
+// exit; registers during the factorization (warp w: rows [w*RW, (w+1)*RW), lane c: column c).
+//   TS (TSTRF): pairwise pivoting of column jj between the top row jj of
+//       UL (32 x 33: U of the slab's diagonal block above the diagonal, the L-strip block
+//       below it, footnote PAPER.md:542-544) and all b rows of P; the top row wins ties
+//       (first maximum in stacked order, Z11).  A swap exchanges the whole 32-entry row.
+//       pivots: b + r + 1 (row r swapped in) or cs + jj + 1 (kept), Z13.
+//   !TS (GETRF): partial pivoting over tile rows >= cs + jj of P (first
+//       maximum), rows swapped over the slab's 32 columns (the caller applies them to the
+//       other columns, Z12); pivots cs-relative rows + 1 in [1, b].
+// Column jj: lane jj's local argmax -> barrier -> every warp merges in warp order -> the
+// rows involved in the swap are published -> barrier -> swap, scaling by the pivot
+// (division, as the oracle), rank-1 update of columns > jj.  Returns the first zero-pivot
+// local column or -1.
+template <int MI, bool TS>
+__device__ inline int lu_panel(double* P, int ldp, int cs, int b, double* UL, int* piv, double* sm2) {
+  constexpr int RW = 8 * MI;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = lane, r0w = warp * RW;
+  double* amv = sm2;                                     // 16 warp maxima
+  int* ami = reinterpret_cast<int*>(amv + 16);           // 16 warp argmax rows
+  double* rowA = amv + 32;                               // 32: pivot row (pre-swap)
+  double* rowB = rowA + 32;                              // 32: GETRF row cs + jj (pre-swap)
+  double* xcol = rowB + 32;                              // 16 x RW: scaled column jj per warp
+  double* xw = xcol + warp * RW;
+  double p[RW];
+#pragma unroll
+  for (int k = 0; k < RW; ++k) p[k] = P[(r0w + k) + (size_t)c * ldp];
+  int first_zero = -1;
+  for (int jj = 0; jj < 32; ++jj) {
+    const int cg = cs + jj;
+    const int kcg = cg - r0w;
+    // lane jj: first maximum of |x| over this warp's candidate rows
+    if (c == jj) {
+      double v = -1.0;
+      int idx = INT_MAX;
+#pragma unroll
+      for (int k = 0; k < RW; ++k)
+        if (TS || k >= kcg) amax_merge(v, idx, fabs(p[k]), r0w + k);
+      amv[warp] = v;
+      ami[warp] = idx;
+    }
+    __syncthreads();
+    double bv = TS ? fabs(UL[jj * 33 + jj]) : -1.0;
+    int pr = TS ? -1 : INT_MAX;
+#pragma unroll
+    for (int w = 0; w < TF_WARPS; ++w) amax_merge(bv, pr, amv[w], ami[w]);
+    if (!TS && pr == INT_MAX) pr = cg;  // (no candidates cannot happen: row cg itself)
+    const int kpr = pr - r0w;
+    // publish the rows the swap exchanges (pre-swap values)
+    if (pr >= 0 && kpr >= 0 && kpr < RW) {
+      double tv = 0.0;
+#pragma unroll
+      for (int k = 0; k < RW; ++k)
+        if (k == kpr) tv = p[k];
+      rowA[c] = tv;
+    }
+    if (!TS && kcg >= 0 && kcg < RW) {
+      double tv = 0.0;
+#pragma unroll
+      for (int k = 0; k < RW; ++k)
+        if (k == kcg) tv = p[k];
+      rowB[c] = tv;
+    }
+    __syncthreads();
+    // the new top / pivot row, and the swap
+    const double oldtop = TS ? UL[jj * 33 + c] : rowB[c];
+    const double newtop = (TS && pr < 0) ? oldtop : rowA[c];
+    const double u = __shfl_sync(0xffffffffu, newtop, jj);
+    if (TS) {
+      if (pr >= 0 && kpr >= 0 && kpr < RW) {
+#pragma unroll
+        for (int k = 0; k < RW; ++k)
+          if (k == kpr) p[k] = oldtop;
+      }
+    } else if (pr != cg) {
+      if (kpr >= 0 && kpr < RW) {
+#pragma unroll
+        for (int k = 0; k < RW; ++k)
+          if (k == kpr) p[k] = oldtop;  // row pr <- row cg
+      }
+      if (kcg >= 0 && kcg < RW) {
+#pragma unroll
+        for (int k = 0; k < RW; ++k)
+          if (k == kcg) p[k] = newtop;  // row cg <- row pr
+      }
+    }
+    if (warp == 0) {
+      if (TS) UL[jj * 33 + c] = newtop;
+      if (c == 0) piv[jj] = TS ? (pr >= 0 ? b + pr + 1 : cg + 1) : pr + 1;
+    }
+    if (u != 0.0) {
+      // multipliers of column jj (rows below the pivot), then the rank-1 update
+      __syncwarp();
+      if (c == jj) {
+#pragma unroll
+        for (int k = 0; k < RW; ++k) {
+          const bool below = TS || k > kcg;
+          if (below) p[k] = p[k] / u;
+          xw[k] = below ? p[k] : 0.0;
+        }
+      }
+      __syncwarp();
+      if (c > jj) {
+#pragma unroll
+        for (int k = 0; k < RW; k += 2) {
+          const double2 x2 = *reinterpret_cast<const double2*>(xw + k);
+          p[k] = fma(-x2.x, newtop, p[k]);
+          p[k + 1] = fma(-x2.y, newtop, p[k + 1]);
+        }
+      }
+    } else if (first_zero < 0) {
+      first_zero = jj;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < RW; ++k) P[(r0w + k) + (size_t)c * ldp] = p[k];
+  __syncthreads();
+  return first_zero;
+}
+
+// TSTRF for ib = 32, left-looking over 32-column slabs: every finished
+// block's pairwise swaps / unit-lower solve / update (lu_ts_apply), then the slab's panel.
+// U: the diagonal tile (upper region only is touched), A: the tile below, Ls: L strip,
+// ipiv: pivots (i,k).  Returns the first zero-pivot local column or -1.
+template <int MI>
+__device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, double* sm) {
+  const int b = cx.b, ib = cx.ib;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+  constexpr int RW = 8 * MI;
+  const int r0 = warp * RW;
+  const int ldp = b + 1;
+  int first_zero = -1;
+  double acc[MI][SNJ][2];
+  for (int cs = 0; cs < b; cs += NSR) {
+    slab_load<MI>(acc, A + (size_t)cs * b, b);
+    for (int c0 = 0; c0 < cs; c0 += ib)
+      lu_ts_apply<MI>(acc, U + c0 + (size_t)cs * b, A + (size_t)c0 * b, Ls + (size_t)c0 * ib, ipiv + c0, ib, b, sm);
+    double* P = sm;
+    double* UL = P + 32 * ldp;
+    double* sm2 = UL + 32 * 33;
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) P[(r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * ldp] = acc[i][j][e];
+    for (int e = tid; e < 32 * 32; e += TF_THREADS) {
+      const int rr = e % 32, cc = e / 32;
+      UL[rr * 33 + cc] = (rr <= cc) ? ldg_cg(U + (cs + rr) + (size_t)(cs + cc) * b) : 0.0;
+    }
+    __syncthreads();
+    const int fz = lu_panel<MI, true>(P, ldp, cs, b, UL, ipiv + cs, sm2);
+    if (fz >= 0 && first_zero < 0) first_zero = cs + fz;
+    for (int e = tid; e < b * 32; e += TF_THREADS) {
+      const int rr = e % b, cc = e / b;
+      A[rr + (size_t)(cs + cc) * b] = P[rr + (size_t)cc * ldp];
+    }
+    for (int e = tid; e < 32 * 32; e += TF_THREADS) {
+      const int rr = e % 32, cc = e / 32;
+      if (rr <= cc) U[(cs + rr) + (size_t)(cs + cc) * b] = UL[rr * 33 + cc];
+      Ls[(size_t)(cs + cc) * ib + rr] = rr > cc ? UL[rr * 33 + cc] : 0.0;
     }
     __syncthreads();
   }
-  slab_store<MI>(acc, C, b);
+  return first_zero;
+}
+
+// GETRF for ib = 32, left-looking over 32-column slabs: the slab gets all
+// earlier row interchanges and block solves/updates, then its panel; the slab's interchanges
+// are then applied to the columns on its left (LAPACK dgetrf semantics, Z12).  LX: explicit
+// unit-lower copy written at the end.  Returns the first zero-pivot local column or -1.
+template <int MI>
+__device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX, double* sm) {
+  const int b = cx.b, ib = cx.ib;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+  constexpr int RW = 8 * MI;
+  const int r0 = warp * RW;
+  const int ldp = b + 1;
+  int first_zero = -1;
+  double acc[MI][SNJ][2];
+  for (int cs = 0; cs < b; cs += NSR) {
+    slab_load<MI>(acc, A + (size_t)cs * b, b);
+    if (cs > 0) {
+      lu_rows_permute<MI>(acc, ipiv, 0, cs, b, sm);
+      for (int c0 = 0; c0 < cs; c0 += ib) lu_rows_block<MI>(acc, A, c0, ib, b, sm);
+    }
+    double* P = sm;
+    double* sm2 = P + 32 * ldp;
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) P[(r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * ldp] = acc[i][j][e];
+    __syncthreads();
+    const int fz = lu_panel<MI, false>(P, ldp, cs, b, nullptr, ipiv + cs, sm2);
+    if (fz >= 0 && first_zero < 0) first_zero = cs + fz;
+    for (int e = tid; e < b * 32; e += TF_THREADS) {
+      const int rr = e % b, cc = e / b;
+      A[rr + (size_t)(cs + cc) * b] = P[rr + (size_t)cc * ldp];
+    }
+    __syncthreads();
+    // this slab's interchanges on the columns to its left (one thread per column)
+    for (int cc = tid; cc < cs; cc += TF_THREADS)
+      for (int j = cs; j < cs + 32; ++j) {
+        const int r = ipiv[j] - 1;
+        if (r != j) {
+          double* col = A + (size_t)cc * b;
+          const double t = col[j];
+          col[j] = col[r];
+          col[r] = t;
+        }
+      }
+    __syncthreads();
+  }
+  for (int e = tid; e < b * b; e += TF_THREADS) {
+    const int r = e % b, cc = e / b;
+    LX[e] = (r > cc) ? A[e] : (r == cc ? 1.0 : 0.0);
+  }
+  return first_zero;
 }
 
 }  // namespace tf

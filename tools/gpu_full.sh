@@ -2,8 +2,9 @@
 mkdir -p gpurun_out
 python -c "import oracle; oracle.build()"
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
-timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -15 | tee gpurun_out/pytest_gpu.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+export TF_DIST_TIMEOUT_S=30
+timeout 1200 python -m pytest tests -q -m gpu 2>&1 | tail -5 | tee gpurun_out/pytest_gpu.log
+timeout 1200 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 tail -3 gpurun_out/bench.err; cat gpurun_out/bench.json
 CMD="python bench.py --steps 1 --warmup 1 --only --no-e2e --no-cpu"
 timeout 600 $CMD > gpurun_out/plain.log 2>&1 && \

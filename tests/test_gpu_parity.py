@@ -91,6 +91,8 @@ def test_chol_not_spd_info():
     (90, 30, 5, 3),       # odd ib
     (512, 512, 64, 4),    # p = 1, panel in global memory (b*ib too large for smem)
     (63, 21, 7, 5),       # odd b
+    (1024, 512, 64, 6),   # config-5 tile shape, p = 2 (T12 coupling, ib = 64)
+    (640, 128, 32, 7),    # b = 128 slab path, p = 5
 ])
 def test_qr_parity(n, b, ib, seed):
     A = tilegen.uniform(n, seed)
@@ -108,7 +110,8 @@ def test_qr_parity(n, b, ib, seed):
     assert np.linalg.norm(A - QR) / np.linalg.norm(A) <= 1e-13
 
 
-@pytest.mark.parametrize("n,b,ib", [(256, 64, 16), (96, 32, 8)])
+@pytest.mark.parametrize("n,b,ib", [(256, 64, 16), (96, 32, 8),
+                                    (384, 128, 32), (512, 256, 32), (512, 512, 64)])  # register-slab sizes
 def test_qr_exact_pins(n, b, ib):
     A, d = tilegen.qr_perm(n, 11)
     G, GT, _, _ = gpu_factor("qr", A, b, ib)
@@ -140,6 +143,8 @@ def _lu_sigma(A, b, ib, O, seed=1234):
     (90, 30, 5, 3),
     (512, 512, 64, 4),    # p = 1 (= GEPP), panel in global memory
     (63, 21, 7, 5),
+    (1024, 512, 32, 6),   # b = 512 slab panels, p = 2
+    (640, 128, 32, 7),    # b = 128 slab path, p = 5
 ])
 def test_lu_parity(n, b, ib, seed):
     A = tilegen.normal(n, seed)
@@ -166,7 +171,8 @@ def test_lu_parity(n, b, ib, seed):
     assert np.linalg.norm(A - NU) / np.linalg.norm(A) <= max(1e-12, 2 * ro)
 
 
-@pytest.mark.parametrize("n,b,ib", [(256, 64, 16), (96, 32, 8), (128, 128, 32)])
+@pytest.mark.parametrize("n,b,ib", [(256, 64, 16), (96, 32, 8), (128, 128, 32),
+                                    (384, 128, 32), (512, 256, 32), (512, 512, 64)])  # register-slab sizes
 def test_lu_exact_pin_bitwise(n, b, ib):
     A, L0, U0 = tilegen.lu_exact(n, 3)
     G, GL, Gp, gi = gpu_factor("lu", A, b, ib)

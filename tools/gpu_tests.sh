@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
 python -c "import oracle; oracle.build()"
-timeout 900 python -m pytest tests/test_gpu_parity.py -q 2>&1 | tail -40 | tee gpurun_out/pytest_gpu1.log
+export TF_DIST_TIMEOUT_S=30
+timeout 2400 python -m pytest tests -q -m gpu -x --durations=8 2>&1 | tail -25 | tee gpurun_out/pytest_gpu_full.log

@@ -416,7 +416,7 @@ int check_args(int64_t n, int64_t b, int64_t ib, const void* dA) {
 // count (multi-GPU: the max over ranks, so `tail` sits at the same offset on every rank).
 void fill_sched(Sched& S, const HostDag& H, const DevDag& D, int* st, int* q, int stride = -1) {
   const int nt = (int)H.tasks.size();
-  const int ns = stride < 0 ? nt : stride;
+  const int ns = ((stride < 0 ? nt : stride) + 3) & ~3;  // head/tail 16-byte aligned (vector loads)
   S.tasks = D.tasks;
   S.succ_off = D.succ_off;
   S.succ = D.succ;
@@ -451,7 +451,7 @@ int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, dou
   W.stream = stream;
   const int nt = (int)H.tasks.size();
   const int ctas = g_ctas > 0 ? g_ctas : g_nsm[dev];
-  const size_t state_ints = (size_t)2 * nt + 2 * NLEV + 8;
+  const size_t state_ints = (size_t)2 * (nt + 4) + 2 * NLEV + 8;
   if ((rc = ensure(W.state, state_ints * sizeof(int)))) return rc;
   if ((rc = ensure(W.q, (size_t)H.nitems * sizeof(int)))) return rc;
   if (alg != 0 && (rc = ensure(W.vx, (size_t)p * b * b * sizeof(double)))) return rc;
@@ -544,7 +544,7 @@ int dist_create(DistRank& X, int alg, int64_t n, int64_t b, int64_t ib, int P, i
   const size_t bb = (size_t)b * b;
   const size_t nslots = pl.nranks > 1 ? (size_t)p * (p + 1) / 2 : 0;
   X.off_state = SY_INTS * sizeof(int);
-  const size_t state_ints = (size_t)2 * pl.max_tasks + 2 * NLEV + 8;
+  const size_t state_ints = (size_t)2 * (pl.max_tasks + 4) + 2 * NLEV + 8;
   X.off_q = align256(X.off_state + state_ints * sizeof(int));
   X.off_ctile = align256(X.off_q + (size_t)pl.max_items * sizeof(int));
   X.off_cstrip = X.off_ctile + nslots * bb * sizeof(double);
@@ -657,7 +657,7 @@ int dist_prepare(DistRank& X, RankRun& RR, int cta0, int nctas, double* dA, doub
   D.vptr = tab + 3 * np2;
   D.sends = X.dag.sends;
   for (int r = 0; r < TF_MAX_RANKS; ++r) D.peer_sym[r] = X.peer_sym[r];
-  D.off_tail = X.off_state + ((size_t)2 * pl.max_tasks + NLEV) * sizeof(int);
+  D.off_tail = X.off_state + ((size_t)2 * ((pl.max_tasks + 3) & ~3) + NLEV) * sizeof(int);
   D.off_q = X.off_q;
   D.off_ctile = X.off_ctile;
   D.off_cstrip = X.off_cstrip;

@@ -282,12 +282,40 @@ struct Gemm {
   template <int VEC>
   __device__ __forceinline__ void run_mb(double* sm, const double* A, int lda, const double* B, int ldb, int M,
                                          int N, int K) {
+    prefill_mb<VEC>(sm, A, lda, B, ldb, M, N, K);
+    main_mb<VEC>(sm, A, lda, B, ldb, M, N, K);
+  }
+
+  // run_mb split in two so that a following GEMM's first slices can be in flight while the
+  // caller stores the previous result (gemm_item's two sub-tiles).  prefill issues the first
+  // NST-1 slices; main_mb runs the k loop; the slice counter lives in `pbase` in between.
+  uint32_t pbase;
+  template <int VEC>
+  __device__ __forceinline__ void prefill_mb(double* sm, const double* A, int lda, const double* B, int ldb, int M,
+                                             int N, int K) {
     uint64_t* full = pipe_bars_c(sm);
     uint64_t* empty = full + NST;
     uint64_t* counter = full + 2 * NST;
     const int nk = (K + KC - 1) / KC;
-    const uint32_t base = (uint32_t)*reinterpret_cast<volatile uint64_t*>(counter);
+    pbase = (uint32_t)*reinterpret_cast<volatile uint64_t*>(counter);
     __syncthreads();  // earlier shared-memory users of the stage buffers are done
+    for (int kt = 0; kt < NST - 1 && kt < nk; ++kt) {
+      const uint32_t g = pbase + kt;
+      const int s = g % NST;
+      const uint32_t use = g / NST;
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      load_slice<VEC>(sm, s, A, lda, B, ldb, M, N, K, kt);
+      cp_async_mbar_arrive(&full[s]);
+    }
+  }
+  template <int VEC>
+  __device__ __forceinline__ void main_mb(double* sm, const double* A, int lda, const double* B, int ldb, int M,
+                                          int N, int K) {
+    uint64_t* full = pipe_bars_c(sm);
+    uint64_t* empty = full + NST;
+    uint64_t* counter = full + 2 * NST;
+    const int nk = (K + KC - 1) / KC;
+    const uint32_t base = pbase;
     auto fill = [&](int kt) {
       const uint32_t g = base + kt;
       const int s = g % NST;
@@ -296,7 +324,6 @@ struct Gemm {
       load_slice<VEC>(sm, s, A, lda, B, ldb, M, N, K, kt);
       cp_async_mbar_arrive(&full[s]);
     };
-    for (int kt = 0; kt < NST - 1 && kt < nk; ++kt) fill(kt);
     const int lane = threadIdx.x & 31;
     for (int kt = 0; kt < nk; ++kt) {
       const uint32_t g = base + kt;
@@ -309,6 +336,19 @@ struct Gemm {
     }
     __syncthreads();
     *reinterpret_cast<volatile uint64_t*>(counter) = base + nk;
+  }
+  __device__ __forceinline__ static bool vec2_ok(const double* A, int lda, const double* B, int ldb) {
+    return ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 && ((lda | ldb) & 1) == 0;
+  }
+  __device__ __forceinline__ void prefill(double* sm, const double* A, int lda, const double* B, int ldb, int M,
+                                          int N, int K) {
+    if (vec2_ok(A, lda, B, ldb)) prefill_mb<2>(sm, A, lda, B, ldb, M, N, K);
+    else prefill_mb<1>(sm, A, lda, B, ldb, M, N, K);
+  }
+  __device__ __forceinline__ void finish(double* sm, const double* A, int lda, const double* B, int ldb, int M,
+                                         int N, int K) {
+    if (vec2_ok(A, lda, B, ldb)) main_mb<2>(sm, A, lda, B, ldb, M, N, K);
+    else main_mb<1>(sm, A, lda, B, ldb, M, N, K);
   }
 
   // Full-tile fast path for m/n-contiguous operands: one elected producer thread streams

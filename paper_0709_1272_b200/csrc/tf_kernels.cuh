@@ -237,25 +237,33 @@ __device__ inline void gemm_item(const Ctx& cx, const double* A, const double* B
                                  double* sm) {
   const int b = cx.b;
   const int nr = ceil_div(b, RB);
-  if (gemm_pairs(b)) {
-    // two 128x128 sub-tiles (same rows, adjacent columns) per item: the second GEMM's first
-    // k-slices are in flight while the first result is stored, and the scheduler round trip
-    // is paid once per two sub-tiles
+  const int gs = gemm_group(b);
+  if (gs > 1) {
+    // gs 128x128 sub-tiles (same rows, adjacent columns) per item: each next GEMM's first
+    // k-slices are in flight while the previous result is stored, and the scheduler round
+    // trip is paid once per group
     const int mi = item % nr, nj = item / nr;
-    const int m0 = mi * RB, n0 = 2 * nj * RB, n1 = n0 + RB;
-    const int mm = min(RB, b - m0), nn0 = min(RB, b - n0), nn1 = min(RB, b - n1);
-    prefetch_l2(C + m0 + (size_t)n0 * b, b, mm, nn0);
-    prefetch_l2(C + m0 + (size_t)n1 * b, b, mm, nn1);
-    {
-      GemmNT128 g;
-      g.zero();
-      g.run(sm, A + m0, b, B + n0, b, mm, nn0, b);
-      GemmNT128 h;
-      h.prefill(sm, A + m0, b, B + n1, b, mm, nn1, b);
-      sub_store(g, C + m0 + (size_t)n0 * b, b, mm, nn0);
-      h.zero();
-      h.finish(sm, A + m0, b, B + n1, b, mm, nn1, b);
-      sub_store(h, C + m0 + (size_t)n1 * b, b, mm, nn1);
+    const int m0 = mi * RB, mm = min(RB, b - m0);
+    for (int x = 0; x < gs; ++x) {
+      const int n = (nj * gs + x) * RB;
+      prefetch_l2(C + m0 + (size_t)n * b, b, mm, min(RB, b - n));
+    }
+    GemmNT128 g;
+    g.zero();
+    g.run(sm, A + m0, b, B + (size_t)nj * gs * RB, b, mm, min(RB, b - nj * gs * RB), b);
+    for (int x = 0; x < gs; ++x) {
+      const int n = (nj * gs + x) * RB, nn = min(RB, b - n);
+      if (x + 1 < gs) {
+        const int n2 = n + RB, nn2 = min(RB, b - n2);
+        GemmNT128 h;
+        h.prefill(sm, A + m0, b, B + n2, b, mm, nn2, b);
+        sub_store(g, C + m0 + (size_t)n * b, b, mm, nn);
+        g.zero();
+        g.pbase = h.pbase;
+        g.finish(sm, A + m0, b, B + n2, b, mm, nn2, b);
+      } else {
+        sub_store(g, C + m0 + (size_t)n * b, b, mm, nn);
+      }
     }
     __syncthreads();
     return;

@@ -38,15 +38,24 @@ TF_HD inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 constexpr int NSR = 32;
 TF_HD inline bool ssrfb_reg_ok(int b, int ib) { return b % 128 == 0 && b <= 512 && ib % 32 == 0 && ib <= 64; }
 
-// GEMM items cover two adjacent 128x128 sub-tiles when the tile has an even number of them
-TF_HD inline bool gemm_pairs(int b) { return b >= 256 && ceil_div(b, RB) % 2 == 0; }
+// GEMM items cover gemm_group(b) adjacent 128x128 sub-tiles of one row strip (TF_GEMM_GROUP
+// caps it; 1 = one sub-tile per item)
+#ifndef TF_GEMM_GROUP
+#define TF_GEMM_GROUP 4
+#endif
+TF_HD inline int gemm_group(int b) {
+  const int nr = ceil_div(b, RB);
+  int gsz = 1;
+  while (gsz * 2 <= TF_GEMM_GROUP && nr % (gsz * 2) == 0) gsz *= 2;
+  return gsz;
+}
 
 TF_HD inline int items_of(int kind, int b, int ib) {
   const int nr = ceil_div(b, RB);
   switch (kind) {
     case 1: return nr;                 // TRSM: row blocks
     case 2: return nr * (nr + 1) / 2;  // SYRK: lower sub-tiles
-    case 3: return gemm_pairs(b) ? nr * nr / 2 : nr * nr;  // GEMM: (pairs of) sub-tiles
+    case 3: return nr * nr / gemm_group(b);  // GEMM: groups of sub-tiles
     case 5: case 7: case 9: case 11: return ssrfb_reg_ok(b, ib) ? b / NSR : ceil_div(b, NS);  // slabs
     default: return 1;                 // panels, RECV
   }

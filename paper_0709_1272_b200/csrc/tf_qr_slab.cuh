@@ -103,7 +103,9 @@ __device__ __forceinline__ void slab_apply(double (&acc)[MI][SNJ][2], const doub
             dmma(pc[mi][j], a[1][mi], b1);
           }
         }
+#ifndef TF_SLAB_NOBOUND
         if (i & 1) asm volatile("" ::: "memory");  // bound load hoisting (register budget)
+#endif
       }
     }
     double* slot = part + (pp & 1) * SPB + warp * 512;

@@ -1,1 +1,1 @@
-for a in "tsqrt 256 32 1 2" "geqrt 256 32 1 2" "tsqrt 512 64 1 1" "geqrt 512 64 1 1"; do ./build/kbench $a; done
+for k in kbench kbench_nb; do echo "$k $(./build/$k ssrfb 512 64 1 2)"; echo "$k $(./build/$k ssrfb 256 32 1 4)"; done

@@ -113,14 +113,26 @@ __device__ inline int chol_diag_block(double* D, int nb, int* sflag) {
     for (int j = 0; j < nb; ++j) {
       double s = 0.0;
       if (lane >= j && lane < nb) {
-        s = D[lane + j * (NB + 1)];
-        for (int m = 0; m < j; ++m) s -= D[lane + m * (NB + 1)] * D[j + m * (NB + 1)];
+        // two interleaved partial sums halve the dependent FMA chain (rounding order only)
+        double s0 = D[lane + j * (NB + 1)], s1 = 0.0;
+        int m = 0;
+        for (; m + 1 < j; m += 2) {
+          s0 -= D[lane + m * (NB + 1)] * D[j + m * (NB + 1)];
+          s1 -= D[lane + (m + 1) * (NB + 1)] * D[j + (m + 1) * (NB + 1)];
+        }
+        if (m < j) s0 -= D[lane + m * (NB + 1)] * D[j + m * (NB + 1)];
+        s = s0 + s1;
       }
       const double d = __shfl_sync(0xffffffffu, s, j);
       if (!(d > 0.0)) { fail = j; break; }
-      const double ljj = sqrt(d);
-      if (lane == j) D[j + j * (NB + 1)] = ljj;
-      else if (lane > j && lane < nb) D[lane + j * (NB + 1)] = s / ljj;
+      // 1/sqrt once per column: L_jj = d * r, L_rj = s * r (no division in the chain)
+      const double r = rsqrt(d);
+      if (lane == j) {
+        D[j + j * (NB + 1)] = d * r;
+        D[NB + j * (NB + 1)] = r;  // padding row: reciprocal of L_jj for row_solve
+      } else if (lane > j && lane < nb) {
+        D[lane + j * (NB + 1)] = s * r;
+      }
       __syncwarp();
     }
     if (lane == 0) *sflag = fail;
@@ -140,7 +152,7 @@ __device__ inline void row_solve(double* X, int ldx, int rows, int nb, const dou
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
       if (c < nb) {
-        x[c] = x[c] / D[c + c * (NB + 1)];
+        x[c] = x[c] * D[NB + c * (NB + 1)];  // reciprocal of the diagonal (padding row)
 #pragma unroll
         for (int c2 = c + 1; c2 < NB; ++c2)
           if (c2 < nb) x[c2] -= x[c] * D[c2 + c * (NB + 1)];
@@ -152,10 +164,15 @@ __device__ inline void row_solve(double* X, int ldx, int rows, int nb, const dou
   }
 }
 
+// (the padding row NB of each column receives 1 / diagonal for row_solve: the row solves
+// multiply by a reciprocal computed once per column instead of dividing in every row's
+// dependency chain; exact whenever the diagonal is a power of two, as in the integer pins)
 __device__ inline void load_lower_block(double* D, const double* A, int ld, int nb) {
   for (int e = threadIdx.x; e < NB * NB; e += TF_THREADS) {
     const int r = e % NB, c = e / NB;
-    D[r + c * (NB + 1)] = (r < nb && c < nb && r >= c) ? ldg_cg(A + r + (size_t)c * ld) : 0.0;
+    const double v = (r < nb && c < nb && r >= c) ? ldg_cg(A + r + (size_t)c * ld) : 0.0;
+    D[r + c * (NB + 1)] = v;
+    if (r == c) D[NB + c * (NB + 1)] = 1.0 / v;
   }
   __syncthreads();
 }

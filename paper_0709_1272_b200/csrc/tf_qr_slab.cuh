@@ -346,24 +346,24 @@ __device__ inline void slab_panel(double* P, int ldp, int cs, double* Rb, double
       const int rr = e / 32, cc = e % 32;
       if (rr <= cc) Rb[rr * 33 + cc] = Rbn[rr * 33 + cc];
     }
-  // T (32 x 32, upper; Ts[m*33 + c] = T(m, c)) by the column recurrence (warp 0)
-  // (uniform trip counts with T(c, m) = 0 for m < c, four independent partial sums)
+  // T (32 x 32, upper; Ts[m*33 + c] = T(m, c)) by the column recurrence, row-parallel on
+  // warp 0: lane c keeps its row of T in registers (fully unrolled, static indices)
+  //   T(c, jj) = -tau_jj sum_{c <= m < jj} T(c, m) sdot_jj[m],  T(c, c) = tau_c
   if (warp == 0) {
+    double t[32];
+#pragma unroll
     for (int jj = 0; jj < 32; ++jj) {
-      const double tj = sTau[jj];
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int m = 0;
-      for (; m + 3 < jj; m += 4) {
-        a0 += Ts[c * 33 + m] * sS[jj * 33 + m];
-        a1 += Ts[c * 33 + m + 1] * sS[jj * 33 + m + 1];
-        a2 += Ts[c * 33 + m + 2] * sS[jj * 33 + m + 2];
-        a3 += Ts[c * 33 + m + 3] * sS[jj * 33 + m + 3];
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int m = 0; m < jj; ++m) {
+        if (m & 1) a1 = fma(t[m], sS[jj * 33 + m], a1);
+        else a0 = fma(t[m], sS[jj * 33 + m], a0);
       }
-      for (; m < jj; ++m) a0 += Ts[c * 33 + m] * sS[jj * 33 + m];
-      const double acc = -tj * ((a0 + a1) + (a2 + a3));
-      Ts[c * 33 + jj] = c < jj ? acc : (c == jj ? tj : 0.0);
-      __syncwarp();
+      const double tj = sTau[jj];
+      t[jj] = c < jj ? -tj * (a0 + a1) : (c == jj ? tj : 0.0);
     }
+#pragma unroll
+    for (int jj = 0; jj < 32; ++jj) Ts[c * 33 + jj] = t[jj];
   }
   __syncthreads();
 }

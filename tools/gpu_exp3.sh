@@ -1,1 +1,1 @@
-for v in NO_T NO_HOUSE NO_UPDATE NO_DOTS; do echo "== $v"; ./build/panel_bench_$v | head -2; done
+for v in BASE NO_DOTS NO_SYNC NO_RED NO_HOUSE NO_UPDATE NO_T; do echo "== $v $(./build/pb_$v | head -2 | tr '\n' ' ')"; done

@@ -108,7 +108,33 @@ def main():
         out["kinds"][name] = {"items": int(m.sum()), "mean_us": float(dur[m].mean()), "max_us": float(dur[m].max()),
                               "gflops_per_sm": float(fl / (dur[m].mean() * 1e-6) / 1e9),
                               "sm_time_share": float(dur[m].sum() / dur.sum())}
-    # panel chain: per step k the end of the panel task
+    # the realised critical chain: from the last task to finish, repeatedly step to the
+    # predecessor that finished last; time on the chain split into task work and waiting
+    tids = rec[:, 0].astype(np.int64)
+    nt = len(d["kind"])
+    tstart = np.full(nt, np.inf)
+    tend = np.zeros(nt)
+    np.minimum.at(tstart, tids, start)
+    np.maximum.at(tend, tids, end)
+    preds = [[] for _ in range(nt)]
+    for u in range(nt):
+        for e in range(d["succ_off"][u], d["succ_off"][u + 1]):
+            preds[int(d["succ"][e])].append(u)
+    t = int(np.argmax(tend))
+    chain = {"tasks": 0, "work_us": {}, "wait_us": 0.0}
+    while True:
+        name = tf.KIND_NAMES[int(d["kind"][t])]
+        chain["tasks"] += 1
+        chain["work_us"][name] = chain["work_us"].get(name, 0.0) + float(tend[t] - tstart[t])
+        if not preds[t]:
+            chain["wait_us"] += float(tstart[t])
+            break
+        p = max(preds[t], key=lambda x: tend[x])
+        chain["wait_us"] += float(max(0.0, tstart[t] - tend[p]))
+        t = p
+    chain["work_us"] = {k: round(v, 1) for k, v in chain["work_us"].items()}
+    chain["wait_us"] = round(chain["wait_us"], 1)
+    out["critical_chain"] = chain
     print(json.dumps(out, indent=1))
     if a.json:
         json.dump(out, open(a.json, "w"), indent=1)

@@ -179,7 +179,7 @@ __device__ inline void load_lower_block(double* D, const double* A, int ld, int 
 
 // POTRF (DPOTF2): blocked left-looking Cholesky of the b x b tile A.
 // Only the lower triangle is read or written (Z2).  Returns -1 or failing local column.
-__device__ inline int potrf_item(const Ctx& cx, double* A, double* sm) {
+__device__ inline int potrf_left(const Ctx& cx, double* A, double* sm) {
   const int b = cx.b;
   double* D = sm + GemmNT32::SMEM_DOUBLES;  // (NB+1) x NB block after the engine buffers
   int* sflag = reinterpret_cast<int*>(D + (NB + 1) * NB);
@@ -204,6 +204,50 @@ __device__ inline int potrf_item(const Ctx& cx, double* A, double* sm) {
     }
     row_solve(A + jb + nb + (size_t)jb * b, b, b - jb - nb, nb, D);
     fence_proxy_async_all();  // the next column block's bulk copies read what was just stored
+    __syncthreads();
+  }
+  return -1;
+}
+
+// POTRF for b a multiple of 128 (>= 256): right-looking over 128-column panels — each panel
+// is factored left-looking in 32-column steps (K limited to the panel), then the trailing
+// lower triangle takes the rank-128 update as 128x128 DMMA tiles (SYRK/GEMM shape, K = 128).
+__device__ inline int potrf_item(const Ctx& cx, double* A, double* sm) {
+  const int b = cx.b;
+  if (b < 256 || b % 128) return potrf_left(cx, A, sm);
+  double* D = sm + GemmNT32::SMEM_DOUBLES;
+  int* sflag = reinterpret_cast<int*>(D + (NB + 1) * NB);
+  for (int J = 0; J < b; J += 128) {
+    for (int jb = J; jb < J + 128; jb += NB) {
+      if (jb > J) {
+        for (int r0 = jb; r0 < b; r0 += 128) {
+          GemmNT32 g;
+          g.zero();
+          const int mm = min(128, b - r0);
+          g.run(sm, A + r0 + (size_t)J * b, b, A + jb + (size_t)J * b, b, mm, NB, jb - J);
+          sub_store(g, A + r0 + (size_t)jb * b, b, mm, NB, /*lower_mask=*/r0 < jb + NB, r0, jb);
+        }
+        __syncthreads();
+      }
+      load_lower_block(D, A + jb + (size_t)jb * b, b, NB);
+      const int fail = chol_diag_block(D, NB, sflag);
+      if (fail >= 0) return jb + fail;
+      for (int e = threadIdx.x; e < NB * NB; e += TF_THREADS) {
+        const int r = e % NB, c = e / NB;
+        if (r >= c) A[jb + r + (size_t)(jb + c) * b] = D[r + c * (NB + 1)];
+      }
+      row_solve(A + jb + NB + (size_t)jb * b, b, b - jb - NB, NB, D);
+      fence_proxy_async_all();
+      __syncthreads();
+    }
+    // trailing lower triangle: C(mi, ni) -= L(mi, J:J+128) L(ni, J:J+128)^T
+    for (int m0 = J + 128; m0 < b; m0 += 128)
+      for (int n0 = J + 128; n0 <= m0; n0 += 128) {
+        GemmNT128 g;
+        g.zero();
+        g.run(sm, A + m0 + (size_t)J * b, b, A + n0 + (size_t)J * b, b, 128, 128, 128);
+        sub_store(g, A + m0 + (size_t)n0 * b, b, 128, 128, /*lower_mask=*/m0 == n0, m0, n0);
+      }
     __syncthreads();
   }
   return -1;

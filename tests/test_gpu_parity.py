@@ -44,6 +44,8 @@ def test_pack_unpack_bitwise(m, n, b):
     (64, 64, 16, 4),      # p = 1
     (16, 1, 1, 5),        # b = 1
     (640, 160, 32, 6),
+    (1536, 512, 64, 7),   # config-4 tile shape, p = 3: right-looking POTRF, GEMM strips
+    (1024, 256, 32, 8),
 ])
 def test_chol_parity(n, b, ib, seed):
     A = tilegen.spd(n, seed)
@@ -65,7 +67,8 @@ def test_chol_parity(n, b, ib, seed):
     assert np.linalg.norm(A - L @ L.T) / np.linalg.norm(A) <= 1e-13
 
 
-@pytest.mark.parametrize("n,b", [(256, 64), (384, 128), (90, 30)])
+@pytest.mark.parametrize("n,b", [(256, 64), (384, 128), (90, 30),
+                                 (768, 256), (1024, 512)])  # right-looking POTRF, 4-sub-tile GEMM strips
 def test_chol_exact_pin_bitwise(n, b):
     A, L0 = tilegen.chol_exact(n, n + b)
     G, _, _, gi = gpu_factor("chol", A, b, b // 2)

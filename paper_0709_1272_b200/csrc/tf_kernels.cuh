@@ -255,7 +255,7 @@ __device__ inline int potrf_item(const Ctx& cx, double* A, double* sm) {
 
 // TRSM (DTRSM): rows [item*RB, +RB) of X <- X L^{-T}, left-looking over
 // column blocks of NB: X[:,cb] -= X[:,<cb] L[cb,<cb]^T (DMMA), then the NB x NB solve.
-__device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int item, double* sm) {
+__device__ inline void trsm_left(const Ctx& cx, const double* L, double* X, int item, double* sm) {
   const int b = cx.b;
   const int r0 = item * RB, rows = min(RB, b - r0);
   double* D = sm + GemmNT32::SMEM_DOUBLES;
@@ -274,6 +274,39 @@ __device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int 
     load_lower_block(D, L + jb + (size_t)jb * b, b, nb);  // (has __syncthreads)
     row_solve(X + (size_t)jb * b, b, rows, nb, D);
     fence_proxy_async_all();  // the next block's bulk copies read the rows just solved
+    __syncthreads();
+  }
+}
+
+// TRSM for b a multiple of 128 (>= 256): right-looking over 128-column panels as POTRF —
+// each panel solved left-looking in 32-column steps (K limited to the panel), then the
+// columns to its right take the rank-128 update as 128x128 DMMA tiles (K = 128).
+__device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int item, double* sm) {
+  const int b = cx.b;
+  if (b < 256 || b % 128) { trsm_left(cx, L, X, item, sm); return; }
+  const int r0 = item * RB, rows = min(RB, b - r0);
+  double* D = sm + GemmNT32::SMEM_DOUBLES;
+  X += r0;
+  for (int J = 0; J < b; J += 128) {
+    for (int jb = J; jb < J + 128; jb += NB) {
+      if (jb > J) {
+        GemmNT32 g;
+        g.zero();
+        g.run(sm, X + (size_t)J * b, b, L + jb + (size_t)J * b, b, rows, NB, jb - J);
+        sub_store(g, X + (size_t)jb * b, b, rows, NB);
+      }
+      load_lower_block(D, L + jb + (size_t)jb * b, b, NB);  // (has __syncthreads)
+      row_solve(X + (size_t)jb * b, b, rows, NB, D);
+      fence_proxy_async_all();
+      __syncthreads();
+    }
+    // columns to the right: X(:, n0:n0+128) -= X(:, J:J+128) L(n0:n0+128, J:J+128)^T
+    for (int n0 = J + 128; n0 < b; n0 += 128) {
+      GemmNT128 g;
+      g.zero();
+      g.run(sm, X + (size_t)J * b, b, L + n0 + (size_t)J * b, b, rows, 128, 128);
+      sub_store(g, X + (size_t)n0 * b, b, rows, 128);
+    }
     __syncthreads();
   }
 }

@@ -32,6 +32,22 @@ __device__ __forceinline__ void lu_block_solve(double* sU, const double* sL, int
   __syncwarp();
 }
 
+#ifdef TF_PROF_LU
+__device__ long long g_lu_prof[16];
+#define TF_LU_T0() long long lu_t_ = clock64()
+#define TF_LU_T(k)                                                       \
+  do {                                                                   \
+    if (threadIdx.x == 0) {                                              \
+      const long long t_ = clock64();                                    \
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g_lu_prof[k]), (unsigned long long)(t_ - lu_t_)); \
+      lu_t_ = t_;                                                        \
+    }                                                                    \
+  } while (0)
+#else
+#define TF_LU_T0() (void)0
+#define TF_LU_T(k) (void)0
+#endif
+
 // One inner block of the pairwise-pivoted update on a register slab (SSSSM step):
 // [U_s; A] <- swaps of block s, U_s <- (I + Ls_s)^{-1} U_s, A -= L[:, s] U_s.
 //   Us  : U rows c0.. of the slab columns, (m, c) at Us[m + c*b] (read, then written back)
@@ -144,7 +160,9 @@ __device__ __forceinline__ void lu_rows_permute(double (&acc)[MI][SNJ][2], const
   const int r0 = warp * RW;
   double* sC = sm;                                        // b x LU_LDW
   int* perm = reinterpret_cast<int*>(sm + 512 * LU_LDW);  // b
+  int* spv = perm + 512;                                  // the interchanges, staged
   for (int r = tid; r < b; r += TF_THREADS) perm[r] = r;
+  for (int j = j0 + tid; j < j1; j += TF_THREADS) spv[j - j0] = ipiv[j];  // (parallel global loads)
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -154,7 +172,7 @@ __device__ __forceinline__ void lu_rows_permute(double (&acc)[MI][SNJ][2], const
   __syncthreads();
   if (tid == 0)
     for (int j = j0; j < j1; ++j) {
-      const int r = ipiv[j] - 1;
+      const int r = spv[j - j0] - 1;
       const int t = perm[j];
       perm[j] = perm[r];
       perm[r] = t;
@@ -274,20 +292,40 @@ __device__ inline int lu_panel(double* P, int ldp, int cs, int b, double* UL, in
     const int cg = cs + jj;
     const int kcg = cg - r0w;
     // lane jj: first maximum of |x| over this warp's candidate rows
+    // (pairwise trees over ordered halves: the left operand holds the lower rows, so taking
+    //  the right one only when strictly larger keeps the first maximum)
     if (c == jj) {
-      double v = -1.0;
-      int idx = INT_MAX;
+      double v[RW];
+      int id[RW];
 #pragma unroll
-      for (int k = 0; k < RW; ++k)
-        if (TS || k >= kcg) amax_merge(v, idx, fabs(p[k]), r0w + k);
-      amv[warp] = v;
-      ami[warp] = idx;
+      for (int k = 0; k < RW; ++k) {
+        v[k] = (TS || k >= kcg) ? fabs(p[k]) : -1.0;
+        id[k] = (TS || k >= kcg) ? r0w + k : INT_MAX;
+      }
+#pragma unroll
+      for (int st = 1; st < RW; st *= 2)
+#pragma unroll
+        for (int k = 0; k < RW; k += 2 * st)
+          if (v[k + st] > v[k]) { v[k] = v[k + st]; id[k] = id[k + st]; }
+      amv[warp] = v[0];
+      ami[warp] = id[0];
     }
     __syncthreads();
-    double bv = TS ? fabs(UL[jj * 33 + jj]) : -1.0;
-    int pr = TS ? -1 : INT_MAX;
+    int pr;
+    {
+      double v[TF_WARPS];
+      int id[TF_WARPS];
 #pragma unroll
-    for (int w = 0; w < TF_WARPS; ++w) amax_merge(bv, pr, amv[w], ami[w]);
+      for (int w = 0; w < TF_WARPS; ++w) { v[w] = amv[w]; id[w] = ami[w]; }
+#pragma unroll
+      for (int st = 1; st < TF_WARPS; st *= 2)
+#pragma unroll
+        for (int w = 0; w < TF_WARPS; w += 2 * st)
+          if (v[w + st] > v[w]) { v[w] = v[w + st]; id[w] = id[w + st]; }
+      double bv = TS ? fabs(UL[jj * 33 + jj]) : -1.0;
+      pr = TS ? -1 : INT_MAX;
+      if (v[0] > bv) { bv = v[0]; pr = id[0]; }
+    }
     if (!TS && pr == INT_MAX) pr = cg;  // (no candidates cannot happen: row cg itself)
     const int kpr = pr - r0w;
     // publish the rows the swap exchanges (pre-swap values)
@@ -334,16 +372,20 @@ __device__ inline int lu_panel(double* P, int ldp, int cs, int b, double* UL, in
     }
     if (u != 0.0) {
       // multipliers of column jj (rows below the pivot), then the rank-1 update
+      // (the divisions run one per lane, not serially on lane jj)
       __syncwarp();
       if (c == jj) {
 #pragma unroll
-        for (int k = 0; k < RW; ++k) {
-          const bool below = TS || k > kcg;
-          if (below) p[k] = p[k] / u;
-          xw[k] = below ? p[k] : 0.0;
-        }
+        for (int k = 0; k < RW; ++k) xw[k] = (TS || k > kcg) ? p[k] : 0.0;
       }
       __syncwarp();
+      if (c < RW) xw[c] = xw[c] / u;
+      __syncwarp();
+      if (c == jj) {
+#pragma unroll
+        for (int k = 0; k < RW; ++k)
+          if (TS || k > kcg) p[k] = xw[k];
+      }
       if (c > jj) {
 #pragma unroll
         for (int k = 0; k < RW; k += 2) {
@@ -375,10 +417,12 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
   const int ldp = b + 1;
   int first_zero = -1;
   double acc[MI][SNJ][2];
+  TF_LU_T0();
   for (int cs = 0; cs < b; cs += NSR) {
     slab_load<MI>(acc, A + (size_t)cs * b, b);
     for (int c0 = 0; c0 < cs; c0 += ib)
       lu_ts_apply<MI>(acc, U + c0 + (size_t)cs * b, A + (size_t)c0 * b, Ls + (size_t)c0 * ib, ipiv + c0, ib, b, sm);
+    TF_LU_T(8);
     double* P = sm;
     double* UL = P + 32 * ldp;
     double* sm2 = UL + 32 * 33;
@@ -393,8 +437,10 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
       UL[rr * 33 + cc] = (rr <= cc) ? ldg_cg(U + (cs + rr) + (size_t)(cs + cc) * b) : 0.0;
     }
     __syncthreads();
+    TF_LU_T(9);
     const int fz = lu_panel<MI, true>(P, ldp, cs, b, UL, ipiv + cs, sm2);
     if (fz >= 0 && first_zero < 0) first_zero = cs + fz;
+    TF_LU_T(10);
     for (int e = tid; e < b * 32; e += TF_THREADS) {
       const int rr = e % b, cc = e / b;
       A[rr + (size_t)(cs + cc) * b] = P[rr + (size_t)cc * ldp];
@@ -405,6 +451,7 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
       Ls[(size_t)(cs + cc) * ib + rr] = rr > cc ? UL[rr * 33 + cc] : 0.0;
     }
     __syncthreads();
+    TF_LU_T(11);
   }
   return first_zero;
 }
@@ -422,11 +469,14 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
   const int ldp = b + 1;
   int first_zero = -1;
   double acc[MI][SNJ][2];
+  TF_LU_T0();
   for (int cs = 0; cs < b; cs += NSR) {
     slab_load<MI>(acc, A + (size_t)cs * b, b);
     if (cs > 0) {
       lu_rows_permute<MI>(acc, ipiv, 0, cs, b, sm);
+      TF_LU_T(0);
       for (int c0 = 0; c0 < cs; c0 += ib) lu_rows_block<MI>(acc, A, c0, ib, b, sm);
+      TF_LU_T(1);
     }
     double* P = sm;
     double* sm2 = P + 32 * ldp;
@@ -437,25 +487,60 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
 #pragma unroll
         for (int e = 0; e < 2; ++e) P[(r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * ldp] = acc[i][j][e];
     __syncthreads();
+    TF_LU_T(2);
     const int fz = lu_panel<MI, false>(P, ldp, cs, b, nullptr, ipiv + cs, sm2);
     if (fz >= 0 && first_zero < 0) first_zero = cs + fz;
+    TF_LU_T(3);
     for (int e = tid; e < b * 32; e += TF_THREADS) {
       const int rr = e % b, cc = e / b;
       A[rr + (size_t)(cs + cc) * b] = P[rr + (size_t)cc * ldp];
     }
     __syncthreads();
-    // this slab's interchanges on the columns to its left (one thread per column)
-    for (int cc = tid; cc < cs; cc += TF_THREADS)
-      for (int j = cs; j < cs + 32; ++j) {
-        const int r = ipiv[j] - 1;
-        if (r != j) {
-          double* col = A + (size_t)cc * b;
-          const double t = col[j];
-          col[j] = col[r];
-          col[r] = t;
+    TF_LU_T(4);
+    // this slab's interchanges on the columns to its left: composed once into the list of
+    // rows that change (new row x <- old row src[x]), then gathered through shared memory
+    if (cs > 0) {
+      int* perm = reinterpret_cast<int*>(sm);  // rows [cs, b)
+      int* chg = perm + 512;                   // changed rows (<= 64)
+      int* src = chg + 64;
+      int* nchg = src + 64;
+      int* spv = nchg + 1;
+      double* buf = sm + 512;                  // n x (column chunk of <= 256)
+      for (int r = cs + tid; r < b; r += TF_THREADS) perm[r - cs] = r;
+      if (tid < 32) spv[tid] = ipiv[cs + tid];
+      if (tid == 0) *nchg = 0;
+      __syncthreads();
+      if (tid == 0)
+        for (int j = cs; j < cs + 32; ++j) {
+          const int r = spv[j - cs] - 1;
+          const int t = perm[j - cs];
+          perm[j - cs] = perm[r - cs];
+          perm[r - cs] = t;
         }
+      __syncthreads();
+      for (int x = cs + tid; x < b; x += TF_THREADS)
+        if (perm[x - cs] != x) {
+          const int k = atomicAdd(nchg, 1);
+          chg[k] = x;
+          src[k] = perm[x - cs];
+        }
+      __syncthreads();
+      const int n = *nchg;
+      for (int cc0 = 0; cc0 < cs; cc0 += 256) {
+        const int nc = min(256, cs - cc0);
+        for (int e = tid; e < n * nc; e += TF_THREADS) {
+          const int x = e % n, cc = cc0 + e / n;
+          buf[e] = A[src[x] + (size_t)cc * b];
+        }
+        __syncthreads();
+        for (int e = tid; e < n * nc; e += TF_THREADS) {
+          const int x = e % n, cc = cc0 + e / n;
+          A[chg[x] + (size_t)cc * b] = buf[e];
+        }
+        __syncthreads();
       }
-    __syncthreads();
+    }
+    TF_LU_T(5);
   }
   for (int e = tid; e < b * b; e += TF_THREADS) {
     const int r = e % b, cc = e / b;

@@ -105,6 +105,18 @@ int main(int argc, char** argv) {
     printf("\n");
   }
 #endif
+#ifdef TF_PROF_LU
+  {
+    long long z[16] = {0}, h[16];
+    cudaMemcpyToSymbol(g_lu_prof, z, sizeof(z));
+    kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps);
+    CK(cudaDeviceSynchronize());
+    cudaMemcpyFromSymbol(h, g_lu_prof, sizeof(h));
+    printf("lu phases us/task:");
+    for (int i = 0; i < 12; ++i) if (h[i]) printf(" [%d] %.1f", i, h[i] / 1.92e3 / grid / reps);
+    printf("\n");
+  }
+#endif
   const double fl_task[] = {b * (double)b * b / 3, (double)b * b * b, (double)b * b * (b + 1.0), 2.0 * b * b * b,
                             4.0 * b * b * b / 3, 2.0 * b * b * b + 3.0 * ib * b * b, 2.0 * b * b * b + (double)ib * b * b,
                             4.0 * b * b * b + (double)ib * b * b, 2.0 * b * b * b / 3, (double)b * b * b,

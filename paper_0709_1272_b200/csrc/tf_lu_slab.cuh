@@ -24,6 +24,22 @@ constexpr int LU_LDW = NSR + 4;  // row stride of U_s / gathered rows in smem (c
 // per warp), right-looking over m.
 __device__ __forceinline__ void lu_block_solve(double* sU, const double* sL, int ib) {
   const int c = threadIdx.x >> 4, l = threadIdx.x & 15;
+  if (ib == 32) {
+    // rows l and l + 16 in registers; row m broadcast by shuffle within the 16-lane group
+    // (same operations in the same order as the loop below)
+    double x0 = sU[l * LU_LDW + c], x1 = sU[(l + 16) * LU_LDW + c];
+    const int base = threadIdx.x & 16;
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      const double xm = __shfl_sync(0xffffffffu, m < 16 ? x0 : x1, base | (m & 15));
+      if (l > m) x0 -= sL[l * 33 + m] * xm;
+      if (l + 16 > m) x1 -= sL[(l + 16) * 33 + m] * xm;
+    }
+    sU[l * LU_LDW + c] = x0;
+    sU[(l + 16) * LU_LDW + c] = x1;
+    __syncwarp();
+    return;
+  }
   for (int m = 0; m < ib; ++m) {
     __syncwarp();
     const double xm = sU[m * LU_LDW + c];

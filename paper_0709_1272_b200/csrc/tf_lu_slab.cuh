@@ -22,24 +22,32 @@ constexpr int LU_LDW = NSR + 4;  // row stride of U_s / gathered rows in smem (c
 // Forward substitution U_s <- (I + L)^{-1} U_s for ib rows x NSR columns held in smem
 // (sU[m*LU_LDW + c]); sL[r*(ib+1) + m] = L(r, m), r > m.  16 lanes per column (two columns
 // per warp), right-looking over m.
-__device__ __forceinline__ void lu_block_solve(double* sU, const double* sL, int ib) {
+template <int R>
+__device__ __forceinline__ void lu_block_solve_reg(double* sU, const double* sL) {
+  // rows l + 16 t (t < R) in registers; row m broadcast by shuffle within the 16-lane group
+  // (the same operations in the same order as the shared-memory loop)
+  constexpr int IB = 16 * R;
   const int c = threadIdx.x >> 4, l = threadIdx.x & 15;
-  if (ib == 32) {
-    // rows l and l + 16 in registers; row m broadcast by shuffle within the 16-lane group
-    // (same operations in the same order as the loop below)
-    double x0 = sU[l * LU_LDW + c], x1 = sU[(l + 16) * LU_LDW + c];
-    const int base = threadIdx.x & 16;
+  const int base = threadIdx.x & 16;
+  double x[R];
 #pragma unroll
-    for (int m = 0; m < 32; ++m) {
-      const double xm = __shfl_sync(0xffffffffu, m < 16 ? x0 : x1, base | (m & 15));
-      if (l > m) x0 -= sL[l * 33 + m] * xm;
-      if (l + 16 > m) x1 -= sL[(l + 16) * 33 + m] * xm;
-    }
-    sU[l * LU_LDW + c] = x0;
-    sU[(l + 16) * LU_LDW + c] = x1;
-    __syncwarp();
-    return;
+  for (int t = 0; t < R; ++t) x[t] = sU[(l + 16 * t) * LU_LDW + c];
+#pragma unroll
+  for (int m = 0; m < IB; ++m) {
+    const double xm = __shfl_sync(0xffffffffu, x[m >> 4], base | (m & 15));
+#pragma unroll
+    for (int t = m >> 4; t < R; ++t)
+      if (l + 16 * t > m) x[t] -= sL[(l + 16 * t) * (IB + 1) + m] * xm;
   }
+#pragma unroll
+  for (int t = 0; t < R; ++t) sU[(l + 16 * t) * LU_LDW + c] = x[t];
+  __syncwarp();
+}
+
+__device__ __forceinline__ void lu_block_solve(double* sU, const double* sL, int ib) {
+  if (ib == 32) { lu_block_solve_reg<2>(sU, sL); return; }
+  if (ib == 64) { lu_block_solve_reg<4>(sU, sL); return; }
+  const int c = threadIdx.x >> 4, l = threadIdx.x & 15;
   for (int m = 0; m < ib; ++m) {
     __syncwarp();
     const double xm = sU[m * LU_LDW + c];

@@ -148,6 +148,7 @@ def _lu_sigma(A, b, ib, O, seed=1234):
     (63, 21, 7, 5),
     (1024, 512, 32, 6),   # b = 512 slab panels, p = 2
     (640, 128, 32, 7),    # b = 128 slab path, p = 5
+    (1024, 512, 64, 8),   # ib = 64 register block solves (GESSM / SSSSM), p = 2
 ])
 def test_lu_parity(n, b, ib, seed):
     A = tilegen.normal(n, seed)

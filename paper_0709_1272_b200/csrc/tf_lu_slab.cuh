@@ -178,15 +178,19 @@ __device__ inline void ssssm_reg(const Ctx& cx, const double* L, const double* L
 // register slab: composed into a gather permutation, applied through shared memory.
 template <int MI>
 __device__ __forceinline__ void lu_rows_permute(double (&acc)[MI][SNJ][2], const int* ipiv, int j0, int j1, int b,
-                                                double* sm) {
+                                                double* sm, int tp = -1) {
   constexpr int RW = 8 * MI;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   const int r0 = warp * RW;
   double* sC = sm;                                        // b x LU_LDW
   int* perm = reinterpret_cast<int*>(sm + 512 * LU_LDW);  // b
   int* spv = perm + 512;                                  // the interchanges, staged
-  for (int r = tid; r < b; r += TF_THREADS) perm[r] = r;
-  for (int j = j0 + tid; j < j1; j += TF_THREADS) spv[j - j0] = ipiv[j];  // (parallel global loads)
+  if (tp >= 0) {
+    if (tid < b) perm[tid] = tp;  // (the caller's running composition, row tid <- row tp)
+  } else {
+    for (int r = tid; r < b; r += TF_THREADS) perm[r] = r;
+    for (int j = j0 + tid; j < j1; j += TF_THREADS) spv[j - j0] = ipiv[j];  // (parallel global loads)
+  }
 #pragma unroll
   for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -194,7 +198,7 @@ __device__ __forceinline__ void lu_rows_permute(double (&acc)[MI][SNJ][2], const
 #pragma unroll
       for (int e = 0; e < 2; ++e) sC[(r0 + 8 * i + g) * LU_LDW + 8 * j + 2 * q + e] = acc[i][j][e];
   __syncthreads();
-  if (tid == 0)
+  if (tid == 0 && tp < 0)
     for (int j = j0; j < j1; ++j) {
       const int r = spv[j - j0] - 1;
       const int t = perm[j];
@@ -493,11 +497,12 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
   const int ldp = b + 1;
   int first_zero = -1;
   double acc[MI][SNJ][2];
+  int tp = tid;  // running composition of the interchanges so far: row tid <- original row tp
   TF_LU_T0();
   for (int cs = 0; cs < b; cs += NSR) {
     slab_load<MI>(acc, A + (size_t)cs * b, b);
     if (cs > 0) {
-      lu_rows_permute<MI>(acc, ipiv, 0, cs, b, sm);
+      lu_rows_permute<MI>(acc, ipiv, 0, cs, b, sm, tp);
       TF_LU_T(0);
       for (int c0 = 0; c0 < cs; c0 += ib) lu_rows_block<MI>(acc, A, c0, ib, b, sm);
       TF_LU_T(1);
@@ -523,15 +528,17 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
     TF_LU_T(4);
     // this slab's interchanges on the columns to its left: composed once into the list of
     // rows that change (new row x <- old row src[x]), then gathered through shared memory
-    if (cs > 0) {
+    if (cs > 0 || cs + NSR < b) {
       int* perm = reinterpret_cast<int*>(sm);  // rows [cs, b)
       int* chg = perm + 512;                   // changed rows (<= 64)
       int* src = chg + 64;
       int* nchg = src + 64;
       int* spv = nchg + 1;
-      double* buf = sm + 512;                  // n x (column chunk of <= 256)
+      int* tpv = spv + 32;                     // b: the running composition
+      double* buf = sm + 1024;                 // n x (column chunk of <= 256)
       for (int r = cs + tid; r < b; r += TF_THREADS) perm[r - cs] = r;
       if (tid < 32) spv[tid] = ipiv[cs + tid];
+      if (tid < b) tpv[tid] = tp;
       if (tid == 0) *nchg = 0;
       __syncthreads();
       if (tid == 0)
@@ -542,6 +549,8 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
           perm[r - cs] = t;
         }
       __syncthreads();
+      if (tid >= cs && tid < b) tp = tpv[perm[tid - cs]];
+      if (cs > 0) {
       for (int x = cs + tid; x < b; x += TF_THREADS)
         if (perm[x - cs] != x) {
           const int k = atomicAdd(nchg, 1);
@@ -562,6 +571,7 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
           A[chg[x] + (size_t)cc * b] = buf[e];
         }
         __syncthreads();
+      }
       }
     }
     TF_LU_T(5);

@@ -51,7 +51,8 @@ typedef struct CUstream_st* tf_stream_t; /* = cudaStream_t; NULL = legacy defaul
 
 #define TF_ERR_CUDA 1     /* a CUDA runtime call failed (see tile_strerror / tile_last_error) */
 #define TF_ERR_NOMEM 2    /* device allocation for library scratch failed */
-#define TF_ERR_NCCL 3     /* reserved (the multi-GPU data path does not use NCCL) */
+/* (code 3 is unused: the multi-GPU data path is device-initiated peer stores over
+ * CUDA IPC mappings, not NCCL; torch.distributed only exchanges the IPC handles) */
 #define TF_ERR_UNSUPPORTED 4 /* configuration not supported by this build */
 
 /* Largest tile size accepted (the in-CTA panel kernels keep O(b) state per thread). */
@@ -165,6 +166,14 @@ int tile_dist_connect(tf_dist_t h, const void* all_ipc);
 int tile_dist_factor(tf_dist_t h, double* dA_loc, double* dAux_loc, int32_t* dIpiv_loc, int32_t* d_info,
                      tf_stream_t stream);
 void tile_dist_close(tf_dist_t h);
+/* IPC path check (tests; no rank waits on another): tile_dist_probe enqueues on `stream`
+ * one system-scope release store of `value` into peer `peer`'s probe slot for this rank
+ * (through the IPC mapping made by tile_dist_connect) plus one system-scope atomic
+ * increment of that peer's probe counter.  tile_dist_probe_read synchronizes the device
+ * and copies this rank's own probe block to host `out`: TF_MAX_RANKS=8 slots (slot r =
+ * the last value rank r stored here, 0 if none) followed by the counter (9 int32). */
+int tile_dist_probe(tf_dist_t h, int peer, int32_t value, tf_stream_t stream);
+int tile_dist_probe_read(tf_dist_t h, int32_t* out);
 /* Elements per rank of the local buffers (same for every rank): which 0 = A (doubles),
  * 1 = T / L strips (doubles), 2 = ipiv (int32).  -1 on invalid arguments. */
 int64_t tile_dist_local_elems(int alg, int64_t n, int64_t b, int64_t ib, int P, int Q, int which);

@@ -71,6 +71,8 @@ def lib():
             "o_ref_gewp": (ctypes.c_int, [i64, dp, ip]),
             "o_chol_residual": (ctypes.c_double, [i64, dp, dp]),
             "o_kernel_flops": (ctypes.c_double, [ctypes.c_int, ctypes.c_double, ctypes.c_double]),
+            "o_decisions_arm": (None, [dp, i64]),
+            "o_decisions_count": (i64, []),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -191,6 +193,32 @@ def lu(tiles: np.ndarray, n: int, b: int, ib: int):
     piv = np.zeros(p * p * b, dtype=np.int32)
     info = lib().o_lu(n, b, ib, _d(tiles), _d(Ls), _i(piv))
     return Ls, piv, info
+
+
+def lu_decisions(tiles: np.ndarray, n: int, b: int, ib: int):
+    """Algorithm 3 as lu(), also returning every pivot decision's (|winner|, |runner-up|)
+    in program order (C5 seed-margin instrumentation; the arithmetic is lu()'s)."""
+    p = n // b
+    cap = p * (p + 1) // 2 * b
+    dec = np.zeros(2 * cap, dtype=np.float64)
+    lib().o_decisions_arm(_d(dec), cap)
+    try:
+        Ls, piv, info = lu(tiles, n, b, ib)
+        nd = lib().o_decisions_count()
+    finally:
+        lib().o_decisions_arm(None, 0)
+    return Ls, piv, info, dec[:2 * min(nd, cap)].reshape(-1, 2)
+
+
+def pivot_margin(dec: np.ndarray, dec_perturbed: np.ndarray) -> float:
+    """min over decisions of (relative gap between the winner and the
+    runner-up) / (relative change of the winner under the input perturbation).  Large
+    = the pivot sequence is robust to rounding-level differences; < ~10 = pivot-fragile."""
+    best, second = dec[:, 0], dec[:, 1]
+    ok = best > 0
+    gap = (best[ok] - np.maximum(second[ok], 0.0)) / best[ok]
+    chg = np.abs(dec_perturbed[ok, 0] - best[ok]) / best[ok]
+    return float(np.min(gap / np.maximum(chg, 2.0 ** -53))) if ok.any() else float("inf")
 
 
 # ---------------------------------------------------------------- checks

@@ -376,6 +376,19 @@ static void o_swap_rows(double* X, int64_t ld, int64_t r1, int64_t r2, int64_t c
   }
 }
 
+/* Pivot-decision recorder — test instrumentation for the C5 seed-margin reading
+ * (DESIGN.md §3): when armed, every pivot decision of o_getrf /
+ * o_tstrf appends (|winner|, |runner-up|) in program order.  It only reads the
+ * candidates after the decision; the arithmetic is unchanged whether armed or not. */
+static double* o_dec = NULL;
+static int64_t o_dec_cap = 0, o_dec_n = 0;
+void o_decisions_arm(double* buf, int64_t cap) { o_dec = buf; o_dec_cap = cap; o_dec_n = 0; }
+int64_t o_decisions_count(void) { return o_dec_n; }
+static void o_dec_push(double best, double second) {
+  if (o_dec && o_dec_n < o_dec_cap) { o_dec[2 * o_dec_n] = best; o_dec[2 * o_dec_n + 1] = second; }
+  if (o_dec) ++o_dec_n;
+}
+
 /* DGETRF: P A = L U with partial pivoting inside the tile, LAPACK
  * dgetrf semantics with block ib (Z12: whole-tile-row swaps).  First argmax of fabs
  * over rows j..b-1 (idamax rule, Z11).  *info gets the first zero-pivot local column
@@ -388,6 +401,12 @@ void o_getrf(int64_t b, int64_t ib, double* A, int32_t* ipiv, int* info) {
       double best = fabs(OE(A, b, j, j));
       for (int64_t rr = j + 1; rr < b; ++rr)
         if (fabs(OE(A, b, rr, j)) > best) { best = fabs(OE(A, b, rr, j)); r = rr; }
+      if (o_dec) {
+        double second = -1.0;
+        for (int64_t rr = j; rr < b; ++rr)
+          if (rr != r && fabs(OE(A, b, rr, j)) > second) second = fabs(OE(A, b, rr, j));
+        o_dec_push(best, second);
+      }
       ipiv[j] = (int32_t)(r + 1);
       if (OE(A, b, r, j) != 0.0) {
         o_swap_rows(A, b, j, r, 0, b);
@@ -452,6 +471,12 @@ void o_tstrf(int64_t b, int64_t ib, double* U, double* A, double* Ls, int32_t* i
       double best = fabs(OE(U, b, j, j));
       for (int64_t rr = 0; rr < b; ++rr)
         if (fabs(OE(A, b, rr, j)) > best) { best = fabs(OE(A, b, rr, j)); r = rr; }
+      if (o_dec) {
+        double second = (r >= 0) ? fabs(OE(U, b, j, j)) : -1.0;
+        for (int64_t rr = 0; rr < b; ++rr)
+          if (rr != r && fabs(OE(A, b, rr, j)) > second) second = fabs(OE(A, b, rr, j));
+        o_dec_push(best, second);
+      }
       if (r >= 0) {
         ipiv[j] = (int32_t)(b + r + 1);
         for (int64_t c = j; c < c1; ++c) {
@@ -701,21 +726,13 @@ double o_chol_residual(int64_t n, const double* A_lo, const double* L) {
   return sqrt(num) / sqrt(den);
 }
 
-/* Leading-order flop counts per task kind. */
+/* Leading-order flop counts of the two update kernels whose costs the paper states
+ * (PAPER.md:655-656 DSSRFB 4b^3 + s b^2, PAPER.md:674 DSSSSM 2b^3 + s b^2; reading Z7).
+ * The other kinds have no printed count and are not provided (NaN). */
 double o_kernel_flops(int kind, double b, double s) {
   switch (kind) {
-    case 0: return b * b * b / 3.0;          /* POTRF */
-    case 1: return b * b * b;                /* TRSM */
-    case 2: return b * b * (b + 1.0);        /* SYRK */
-    case 3: return 2.0 * b * b * b;          /* GEMM */
-    case 4: return 4.0 * b * b * b / 3.0;    /* GEQRT */
-    case 5: return 2.0 * b * b * b + 3.0 * s * b * b;  /* LARFB (approx.) */
-    case 6: return 2.0 * b * b * b + s * b * b;        /* TSQRT */
     case 7: return 4.0 * b * b * b + s * b * b;        /* SSRFB */
-    case 8: return 2.0 * b * b * b / 3.0;    /* GETRF */
-    case 9: return b * b * b;                /* GESSM */
-    case 10: return b * b * b + s * b * b / 2.0;       /* TSTRF */
     case 11: return 2.0 * b * b * b + s * b * b;       /* SSSSM */
-    default: return 0.0;
+    default: return NAN;
   }
 }

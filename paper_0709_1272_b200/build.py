@@ -3,8 +3,9 @@
     python -m paper_0709_1272_b200.build [--force]
 
 The library statically links the CUDA runtime so the host-only entry points (task-graph
-export, argument validation) load on machines without a GPU.  NCCL is loaded lazily
-with dlopen by the multi-GPU entry points (tf_dist.cpp), so it is not a link dependency.
+export, argument validation) load on machines without a GPU.  It has no NCCL
+dependency: the multi-GPU data path is device-initiated stores into peers' CUDA-IPC
+mapped memory (tf_device.cu), and the handles are exchanged by the caller.
 """
 from __future__ import annotations
 
@@ -64,7 +65,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     tag = "default" if not defines else "_".join(d.replace("=", "-") for d in defines)
     odir = os.path.join(ROOT, "build", "obj", tag)
     os.makedirs(odir, exist_ok=True)
-    objs, logs = [], []
+    objs, logs, todo = [], {}, []
     for src in sources():
         obj = os.path.join(odir, os.path.basename(src) + ".o")
         objs.append(obj)
@@ -72,8 +73,12 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
                                                      for d in _obj_deps(src)):
             log = obj + ".log"
             if os.path.exists(log):
-                logs.append(open(log).read())
+                logs[src] = open(log).read()
             continue
+        todo.append((src, obj))
+
+    def compile_one(job):
+        src, obj = job
         tmp = obj + f".tmp{os.getpid()}"
         cmd = ["nvcc", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", "-o", tmp, src,
                "-I", os.path.join(ROOT, "include")]
@@ -83,8 +88,15 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
             raise RuntimeError(f"nvcc compile of {os.path.basename(src)} failed")
         with open(obj + ".log", "w") as f:
             f.write(r.stderr)
-        logs.append(r.stderr)
         os.replace(tmp, obj)
+        return src, r.stderr
+
+    # the translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, len(todo))) as ex:
+        for src, log in ex.map(compile_one, todo):
+            logs[src] = log
+    logs = [logs[s] for s in sources() if s in logs]
     tmp = lib + f".tmp{os.getpid()}"
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
            "-Xcompiler", "-fPIC", "-o", tmp, *objs, "-ldl"]

@@ -360,7 +360,17 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tf_persistent(const __grid_cons
         }
         st_release_sys(me + SY_GO, D.epoch);
       } else {
-        while (ld_acquire_sys(me + SY_GO) - D.epoch < 0) __nanosleep(64);
+        // the same protocol timeout as wait_all: a leader that never arrives becomes
+        // info = -1 and an abort, not a hung GPU
+        const long long t0 = globaltimer();
+        while (ld_acquire_sys(me + SY_GO) - D.epoch < 0) {
+          if (D.timeout_ns > 0 && globaltimer() - t0 > D.timeout_ns) {
+            atomicExch(P.info, -1);
+            atomicExch(S.abort_flag, 1);
+            break;
+          }
+          __nanosleep(64);
+        }
       }
     }
     __syncthreads();
@@ -441,46 +451,6 @@ __global__ void tf_sched_seed(Sched S, const int* roots, int nroots) {
     for (int r = 0; r < nroots; ++r) sched_push(S, roots[r]);
 }
 
-// Per-kernel test launcher: one CTA per work item of a single task.
-__global__ void __launch_bounds__(TF_THREADS, 1)
-    tk_kernel(int kind, int b, int ib, double* t0, double* t1, double* t2, double* aux, int* ipiv, double* vx,
-              double* scratch, size_t scr_stride, int* info) {
-  extern __shared__ __align__(16) double sm[];
-  Ctx cx;
-  cx.b = b;
-  cx.ib = ib;
-  cx.scratch = scratch + (size_t)blockIdx.x * scr_stride;
-  cx.info = info;
-  cx.abort_flag = nullptr;
-  pipe_init(sm);
-  const int sub = blockIdx.x;
-  int f = -1;
-  switch (kind) {
-    case 0: f = potrf_item(cx, t0, sm); break;
-    case 1: trsm_item(cx, t0, t1, sub, sm); break;
-    case 2: syrk_item(cx, t0, t1, sub, sm); break;
-    case 3: gemm_item(cx, t0, t1, t2, sub, sm); break;
-    case 4: geqrt_item(cx, t0, aux, vx, sm); break;
-    case 5: larfb_item(cx, vx, aux, t1, sub, sm); break;
-    case 6: tsqrt_item(cx, t0, t1, aux, sm); break;
-    case 7: ssrfb_item(cx, t0, aux, t1, t2, sub, sm); break;
-    case 8: f = getrf_item(cx, t0, ipiv, vx, sm); break;
-    case 9: gessm_item(cx, vx, ipiv, t1, sub, sm); break;
-    case 10: f = tstrf_item(cx, t0, t1, aux, ipiv, sm); break;
-    case 11: ssssm_item(cx, t0, aux, ipiv, t1, t2, sub, sm); break;
-  }
-  if (info && threadIdx.x == 0 && blockIdx.x == 0) *info = (f >= 0) ? f + 1 : 0;
-}
-
-// unit-lower explicit copy (V_kk / L_kk) of a factored diagonal tile, for tk_run
-__global__ void unit_lower_kernel(const double* A, double* X, int b) {
-  const size_t bb = (size_t)b * b;
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < bb; e += (size_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e % b), c = (int)(e / b);
-    X[e] = (r > c) ? A[e] : (r == c ? 1.0 : 0.0);
-  }
-}
-
 __global__ void pack_kernel(int64_t m, int64_t n, int64_t b, double* D, double* T, int dir) {
   const int64_t p = m / b;
   const int64_t tot = m * n;
@@ -495,6 +465,15 @@ __global__ void pack_kernel(int64_t m, int64_t n, int64_t b, double* D, double* 
   }
 }
 
+// IPC path check (tile_dist_probe): one system-scope release store of `value` into the
+// peer's probe slot for this rank and one system-scope atomic on its probe counter.
+__global__ void probe_kernel(int* peer_sync, int rank, int value) {
+  if (threadIdx.x == 0) {
+    st_release_sys(peer_sync + SY_PROBE + rank, value);
+    atomicAdd_system(peer_sync + SY_PROBE_CNT, 1);
+  }
+}
+
 // ------------------------------------------------------------------ launch wrappers
 size_t smem_bytes() { return (size_t)SMEM_DOUBLES * sizeof(double); }
 
@@ -503,7 +482,7 @@ static int ok_or(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
 int device_kernel_setup(size_t smem) {
   cudaError_t e = cudaFuncSetAttribute(tf_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
-  return ok_or(cudaFuncSetAttribute(tk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return tk_kernel_setup(smem);
 }
 
 int launch_sched_reset(const Sched& S, const int* indeg0, int qtotal, int* info, void* stream) {
@@ -514,18 +493,19 @@ int launch_sched_seed(const Sched& S, const int* roots, int nroots, void* stream
   tf_sched_seed<<<1, 32, 0, (cudaStream_t)stream>>>(S, roots, nroots);
   return ok_or(cudaGetLastError());
 }
-int launch_persistent(const Runs& R, int ctas, size_t smem, void* stream) {
-  tf_persistent<<<ctas, TF_THREADS, smem, (cudaStream_t)stream>>>(R);
-  return ok_or(cudaGetLastError());
+// coop: cooperative launch (all CTAs guaranteed co-resident or the launch fails), used
+// whenever CTAs wait on one another (multi-rank barriers, emulated ranks).
+int launch_persistent(const Runs& R, int ctas, size_t smem, void* stream, bool coop) {
+  if (!coop) {
+    tf_persistent<<<ctas, TF_THREADS, smem, (cudaStream_t)stream>>>(R);
+    return ok_or(cudaGetLastError());
+  }
+  void* args[] = {const_cast<Runs*>(&R)};
+  return ok_or(cudaLaunchCooperativeKernel((const void*)tf_persistent, dim3(ctas), dim3(TF_THREADS), args, smem,
+                                           (cudaStream_t)stream));
 }
-int launch_tk(int kind, int b, int ib, double* t0, double* t1, double* t2, double* aux, int* ipiv, double* vx,
-              double* scratch, size_t scr_stride, int* info, int items, size_t smem, void* stream) {
-  tk_kernel<<<items, TF_THREADS, smem, (cudaStream_t)stream>>>(kind, b, ib, t0, t1, t2, aux, ipiv, vx, scratch,
-                                                               scr_stride, info);
-  return ok_or(cudaGetLastError());
-}
-int launch_unit_lower(const double* A, double* X, int b, void* stream) {
-  unit_lower_kernel<<<64, 256, 0, (cudaStream_t)stream>>>(A, X, b);
+int launch_probe(char* peer_sym, int rank, int value, void* stream) {
+  probe_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(reinterpret_cast<int*>(peer_sym), rank, value);
   return ok_or(cudaGetLastError());
 }
 int launch_pack(int64_t m, int64_t n, int64_t b, double* D, double* T, int dir, void* stream) {

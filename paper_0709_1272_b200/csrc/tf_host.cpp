@@ -436,6 +436,16 @@ void fill_sched(Sched& S, const HostDag& H, const DevDag& D, int* st, int* q, in
   S.trace_cap = 0;
 }
 
+// Single-GPU scheduler watchdog: no CTA of the one-GPU kernel waits for a specific task,
+// so the only way it can stall is a lost queue push (a bug); if no item can be popped for
+// TF_WATCHDOG_S seconds (default 60, far above the longest item, ~3.3 ms) the kernel
+// aborts with info = -1 instead of hanging the GPU.  0 disables it.
+long long watchdog_ns() {
+  const char* e = getenv("TF_WATCHDOG_S");
+  const double s = e ? atof(e) : 60.0;
+  return s > 0 ? (long long)(s * 1e9) : 0;
+}
+
 int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, double* aux, int32_t* ipiv,
                       int32_t* d_info, cudaStream_t stream) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
@@ -479,9 +489,10 @@ int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, dou
   P.ib = (int)ib;
   P.p = p;
   P.info = d_info ? d_info : (int*)W.info.p;
+  R.r[0].D.timeout_ns = watchdog_ns();
   TF_LAUNCH(launch_sched_reset(S, D->indeg0, H.nitems, P.info, stream));
   TF_LAUNCH(launch_sched_seed(S, D->roots, (int)H.roots.size(), stream));
-  TF_LAUNCH(launch_persistent(R, ctas, smem_bytes(), stream));
+  TF_LAUNCH(launch_persistent(R, ctas, smem_bytes(), stream, false));
   g_last_ws = &W;
   return 0;
 }
@@ -968,7 +979,25 @@ int tile_dist_factor(tf_dist_t h, double* dA_loc, double* dAux_loc, int32_t* dIp
   R.nruns = 1;
   int rc;
   if ((rc = dist_prepare(X, R.r[0], 0, ctas, dA_loc, dAux_loc, dIpiv_loc, d_info, s))) return rc;
-  TF_LAUNCH(launch_persistent(R, ctas, smem_bytes(), s));
+  TF_LAUNCH(launch_persistent(R, ctas, smem_bytes(), s, true));
+  return 0;
+}
+
+int tile_dist_probe(tf_dist_t h, int peer, int32_t value, tf_stream_t stream) {
+  if (!h) return -1;
+  DistRank& X = h->r;
+  if (peer < 0 || peer >= X.plan->nranks || !X.peer_sym[peer]) { set_err("peer %d not mapped", peer); return -2; }
+  TF_LAUNCH(launch_probe(X.peer_sym[peer], X.rank, value, (cudaStream_t)stream));
+  return 0;
+}
+
+int tile_dist_probe_read(tf_dist_t h, int32_t* out) {
+  if (!h) return -1;
+  if (!out) return -2;
+  DistRank& X = h->r;
+  TF_CUDA(cudaDeviceSynchronize());
+  TF_CUDA(cudaMemcpy(out, (char*)X.sym.p + SY_PROBE * sizeof(int), (TF_MAX_RANKS + 1) * sizeof(int),
+                     cudaMemcpyDeviceToHost));
   return 0;
 }
 
@@ -1021,7 +1050,7 @@ int tile_dist_emulate(int alg, int64_t n, int64_t b, int64_t ib, int P, int Q, d
                            dIpiv_loc ? dIpiv_loc[r] : nullptr, r == 0 ? d_info : nullptr, s)))
       return rc;
   }
-  TF_LAUNCH(launch_persistent(RUN, ctas, smem_bytes(), s));
+  TF_LAUNCH(launch_persistent(RUN, ctas, smem_bytes(), s, true));
   return 0;
 }
 
@@ -1031,7 +1060,6 @@ const char* tile_strerror(int code) {
     case 0: return "success";
     case TF_ERR_CUDA: return "CUDA runtime error";
     case TF_ERR_NOMEM: return "device allocation failed";
-    case TF_ERR_NCCL: return "NCCL error";
     case TF_ERR_UNSUPPORTED: return "unsupported configuration";
     default: return code < 0 ? "invalid argument" : "unknown error";
   }

@@ -550,6 +550,7 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
         }
       __syncthreads();
       if (tid >= cs && tid < b) tp = tpv[perm[tid - cs]];
+      __syncthreads();  // perm / tpv are read above; the next slab's permute rewrites this smem
       if (cs > 0) {
       for (int x = cs + tid; x < b; x += TF_THREADS)
         if (perm[x - cs] != x) {

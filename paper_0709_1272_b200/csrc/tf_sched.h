@@ -36,7 +36,8 @@ TF_HD inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 // Register-slab kernels (tf_qr_slab.cuh: SSRFB / LARFB items of NSR columns, slab-wise
 // GEQRT / TSQRT; tf_lu_slab.cuh: GESSM / SSSSM items): b in {128, 256, 512}, ib in {32, 64}.
 constexpr int NSR = 32;
-TF_HD inline bool ssrfb_reg_ok(int b, int ib) { return b % 128 == 0 && b <= 512 && ib % 32 == 0 && ib <= 64; }
+// (exactly the tile sizes TF_SLAB_DISPATCH instantiates: MI = b/128 in {1, 2, 4})
+TF_HD inline bool ssrfb_reg_ok(int b, int ib) { return (b == 128 || b == 256 || b == 512) && (ib == 32 || ib == 64); }
 
 // GEMM items cover gemm_group(b) adjacent 128x128 sub-tiles of one row strip (TF_GEMM_GROUP
 // caps it; 1 = one sub-tile per item)
@@ -105,7 +106,9 @@ struct SendEnt {
 
 // Symmetric per-rank block ("sym"), identical offsets on every rank:
 //   [sync ints][sched state ints][queue ints][cache tiles][cache strips][cache ipiv]
-enum SyncSlot { SY_ARRIVE = 0, SY_DEPART = 8, SY_INFO = 16, SY_GO = 24, SY_ABORT = 25, SY_LINFO = 26, SY_INTS = 32 };
+// SY_PROBE[r] / SY_PROBE_CNT: written by peers' tile_dist_probe (IPC path check, no waiting)
+enum SyncSlot { SY_ARRIVE = 0, SY_DEPART = 8, SY_INFO = 16, SY_GO = 24, SY_ABORT = 25, SY_LINFO = 26,
+                SY_PROBE = 32, SY_PROBE_CNT = 40, SY_INTS = 48 };
 
 struct Dist {
   int nranks;        // 0 = single-GPU mode (direct BDL addressing, no barriers)
@@ -143,12 +146,14 @@ TF_HD inline long long cache_slot(int i, int k, int p) {
 // launch wrappers (tf_device.cu)
 int launch_sched_reset(const Sched& S, const int* indeg0, int qtotal, int* info, void* stream);
 int launch_sched_seed(const Sched& S, const int* roots, int nroots, void* stream);
-int launch_persistent(const Runs& R, int ctas, size_t smem, void* stream);
+int launch_persistent(const Runs& R, int ctas, size_t smem, void* stream, bool coop);
 int launch_tk(int kind, int b, int ib, double* t0, double* t1, double* t2, double* aux, int* ipiv, double* vx,
               double* scratch, size_t scr_stride, int* info, int items, size_t smem, void* stream);
 int launch_unit_lower(const double* A, double* X, int b, void* stream);
 int launch_pack(int64_t m, int64_t n, int64_t b, double* D, double* T, int dir, void* stream);
+int launch_probe(char* peer_sym, int rank, int value, void* stream);
 int device_kernel_setup(size_t smem);
+int tk_kernel_setup(size_t smem);
 size_t smem_bytes();
 
 }  // namespace tf

@@ -51,6 +51,8 @@ def _load():
         "tile_dist_connect": (i32, [vp, vp]),
         "tile_dist_factor": (i32, [vp, vp, vp, vp, vp, vp]),
         "tile_dist_close": (None, [vp]),
+        "tile_dist_probe": (i32, [vp, i32, i32, vp]),
+        "tile_dist_probe_read": (i32, [vp, vp]),
         "tile_dist_local_elems": (i64, [i32, i64, i64, i64, i32, i32, i32]),
         "tile_dist_owner": (i32, [i64, i64, i32, i32]),
         "tile_dist_emulate": (i32, [i32, i64, i64, i64, i32, i32, vp, vp, vp, vp, vp]),
@@ -73,6 +75,7 @@ SYMBOLS = [
     "tile_pack", "tile_unpack", "tile_factor_host", "tile_set_policy", "tile_set_trace",
     "tile_trace_fetch", "tile_set_ctas", "tile_dag_export", "tk_run", "tile_dist_open",
     "tile_dist_ipc_bytes", "tile_dist_connect", "tile_dist_factor", "tile_dist_close",
+    "tile_dist_probe", "tile_dist_probe_read",
     "tile_dist_local_elems", "tile_dist_owner", "tile_dist_emulate", "tile_dist_plan_export",
     "tile_strerror", "tile_last_error", "tile_finalize",
 ]
@@ -95,29 +98,46 @@ def _check(rc: int, what: str):
                             f"{lib.tile_last_error().decode()}")
 
 
-def _dev_f64(t, name):
+def _dev_f64(t, name, numel=None):
+    _dev(t, name, "float64", numel)
+
+
+def _dev(t, name, dtype, numel=None):
+    """The C-ABI takes no buffer lengths: check device, dtype, contiguity and size here so
+    an undersized or mistyped tensor is an error, not an out-of-bounds device write."""
     import torch
-    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
-        raise TileFactError(f"{name} must be a contiguous float64 CUDA tensor")
+    want = {"float64": torch.float64, "int32": torch.int32}[dtype]
+    if t is None or not (t.is_cuda and t.dtype == want and t.is_contiguous()):
+        raise TileFactError(f"{name} must be a contiguous {dtype} CUDA tensor")
+    if numel is not None and t.numel() < numel:
+        raise TileFactError(f"{name} holds {t.numel()} elements, needs {numel}")
+
+
+def _info(info):
+    if info is not None:
+        _dev(info, "info", "int32", 1)
 
 
 # ------------------------------------------------------------------ factorizations
 
 def tile_chol(n, b, ib, A, info=None, stream=None) -> None:
     """In-place tiled Cholesky of the BDL matrix A (n*n doubles on the device)."""
-    _dev_f64(A, "A")
+    _dev_f64(A, "A", n * n)
+    _info(info)
     _check(lib.tile_chol(n, b, ib, _ptr(A), _ptr(info), _stream(stream)), "tile_chol")
 
 
 def tile_qr(n, b, ib, A, T, stream=None) -> None:
-    _dev_f64(A, "A")
-    _dev_f64(T, "T")
+    _dev_f64(A, "A", n * n)
+    _dev_f64(T, "T", tile_qr_t_elems(n, b, ib))
     _check(lib.tile_qr(n, b, ib, _ptr(A), _ptr(T), _stream(stream)), "tile_qr")
 
 
 def tile_lu(n, b, ib, A, Ls, ipiv, info=None, stream=None) -> None:
-    _dev_f64(A, "A")
-    _dev_f64(Ls, "Ls")
+    _dev_f64(A, "A", n * n)
+    _dev_f64(Ls, "Ls", tile_lu_l_elems(n, b, ib))
+    _dev(ipiv, "ipiv", "int32", tile_lu_ipiv_elems(n, b))
+    _info(info)
     _check(lib.tile_lu(n, b, ib, _ptr(A), _ptr(Ls), _ptr(ipiv), _ptr(info), _stream(stream)), "tile_lu")
 
 
@@ -136,10 +156,14 @@ def tile_lu_ipiv_elems(n, b) -> int:
 def tile_pack(m, n, b, dense, tiles, stream=None) -> None:
     """dense: device float64 holding a column-major m x n matrix (e.g. torch tensor of
     shape (n, m) in row-major = column-major (m, n))."""
+    _dev_f64(dense, "dense", m * n)
+    _dev_f64(tiles, "tiles", m * n)
     _check(lib.tile_pack(m, n, b, _ptr(dense), _ptr(tiles), _stream(stream)), "tile_pack")
 
 
 def tile_unpack(m, n, b, tiles, dense, stream=None) -> None:
+    _dev_f64(tiles, "tiles", m * n)
+    _dev_f64(dense, "dense", m * n)
     _check(lib.tile_unpack(m, n, b, _ptr(tiles), _ptr(dense), _stream(stream)), "tile_unpack")
 
 
@@ -244,9 +268,26 @@ class DistHandle:
             _check(lib.tile_dist_connect(self._h, blob), "tile_dist_connect")
 
     def factor(self, A_loc, aux_loc=None, ipiv_loc=None, info=None, stream=None) -> None:
-        _dev_f64(A_loc, "A_loc")
+        args = (self.alg, self.n, self.b, self.ib, self.P, self.Q)
+        _dev_f64(A_loc, "A_loc", tile_dist_local_elems(*args, 0))
+        if self.alg != 0:
+            _dev_f64(aux_loc, "aux_loc", tile_dist_local_elems(*args, 1))
+        if self.alg == 2:
+            _dev(ipiv_loc, "ipiv_loc", "int32", tile_dist_local_elems(*args, 2))
+        _dev(info, "info", "int32", 1)
         _check(lib.tile_dist_factor(self._h, _ptr(A_loc), _ptr(aux_loc), _ptr(ipiv_loc), _ptr(info),
                                     _stream(stream)), "tile_dist_factor")
+
+    def probe(self, peer, value, stream=None) -> None:
+        """IPC path check: store `value` into peer's probe slot for this rank (no waiting)."""
+        _check(lib.tile_dist_probe(self._h, peer, value, _stream(stream)), "tile_dist_probe")
+
+    def probe_read(self):
+        """(slots[8], counter) of this rank's own probe block (synchronizes the device)."""
+        import numpy as np
+        out = np.zeros(9, dtype=np.int32)
+        _check(lib.tile_dist_probe_read(self._h, ctypes.c_void_p(out.ctypes.data)), "tile_dist_probe_read")
+        return out[:8], int(out[8])
 
     def close(self) -> None:
         if self._h:

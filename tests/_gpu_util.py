@@ -90,3 +90,47 @@ def tile_errors(alg, G, O, n, b):
                 g, o = np.tril(g), np.tril(o)
             errs[(i, j)] = rel(g, o)
     return errs
+
+
+# ------------------------------------------------------------------ LU reference with C5 certification
+
+MARGIN_MIN = 100.0   # parity runs use seeds whose pivot margin is >= 100
+
+
+def lu_certified(n, b, ib, seed, gen=None, tries=6):
+    """Oracle LU of a seeded N(0,1) matrix plus the C5 self-spread run.
+
+    The oracle is re-run on A o (1 + 2^-52 xi), xi ~ N(0,1).  The
+    reading requires that perturbed run to keep the SAME pivots; if it does not, or the
+    pivot margin (oracle.pivot_margin) is below MARGIN_MIN, the seed is pivot-fragile:
+    it is reported and the next seed (seed + 1000) is used.  Returns a dict with the
+    accepted seed, the input, the oracle factors, the perturbed factors, the margin and
+    the list of rejected (seed, reason) pairs."""
+    import tilegen
+    gen = gen or tilegen.normal
+    rejected = []
+    for t in range(tries):
+        sd = seed + 1000 * t
+        A = gen(n, sd)
+        F = oracle.pack(A, b)
+        OL, Op, oi, dec = oracle.lu_decisions(F, n, b, ib)
+        r = np.random.default_rng(1234 + sd)
+        Ap = A * (1.0 + 2.0 ** -52 * r.standard_normal(A.shape))
+        Fp = oracle.pack(Ap, b)
+        PL, Pp, _, decp = oracle.lu_decisions(Fp, n, b, ib)
+        if not np.array_equal(Pp, Op):
+            rejected.append((sd, "perturbed oracle flips a pivot"))
+            continue
+        m = oracle.pivot_margin(dec, decp)
+        if m < MARGIN_MIN:
+            rejected.append((sd, f"pivot margin {m:.3g} < {MARGIN_MIN}"))
+            continue
+        print(f"[C5] n={n} b={b} ib={ib}: seed {sd} pivot margin {m:.3g}; rejected {rejected}")
+        return dict(seed=sd, A=A, O=F, OL=OL, Op=Op, info=oi, P=Fp, PL=PL, margin=m, rejected=rejected)
+    raise AssertionError(f"no pivot-robust seed found: {rejected}")
+
+
+def lu_tile_tolerances(cert, n, b):
+    """Per-tile tolerance max(1e-10, 10 sigma_t), sigma_t = the oracle's own spread."""
+    sig = tile_errors("lu", cert["P"], cert["O"], n, b)
+    return {k: max(1e-10, 10 * v) for k, v in sig.items()}, sig

@@ -16,7 +16,8 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
-from _gpu_util import gpu_factor, gpu_pack, oracle_factor, tile_errors, strip, tile, rel  # noqa: E402
+from _gpu_util import (gpu_factor, gpu_pack, lu_certified, lu_tile_tolerances, oracle_factor,  # noqa: E402
+                       rel, strip, tile, tile_errors)
 from paper_0709_1272_b200 import tilefact as tf  # noqa: E402
 
 TOL = 1e-10
@@ -96,6 +97,8 @@ def test_chol_not_spd_info():
     (63, 21, 7, 5),       # odd b
     (1024, 512, 64, 6),   # config-5 tile shape, p = 2 (T12 coupling, ib = 64)
     (640, 128, 32, 7),    # b = 128 slab path, p = 5
+    (1536, 512, 64, 8),   # config-5 tile shape, p = 3: chained TSQRT / SSRFB with i > k + 1
+    (768, 384, 32, 9),    # b = 384: reference-blocked kernels (not a register-slab size)
 ])
 def test_qr_parity(n, b, ib, seed):
     A = tilegen.uniform(n, seed)
@@ -131,14 +134,6 @@ def test_qr_exact_pins(n, b, ib):
 
 # ------------------------------------------------------------------ LU
 
-def _lu_sigma(A, b, ib, O, seed=1234):
-    """Oracle self-spread per tile under a 2^-52 relative perturbation (C5 reading)."""
-    r = np.random.default_rng(seed)
-    Ap = A * (1.0 + 2.0 ** -52 * r.standard_normal(A.shape))
-    Op, _, pp, _ = oracle_factor("lu", Ap, b, ib)
-    return Op, pp
-
-
 @pytest.mark.parametrize("n,b,ib,seed", [
     (768, 256, 32, 0),    # config-3 tile shape, p = 3
     (512, 128, 16, 1),
@@ -149,12 +144,14 @@ def _lu_sigma(A, b, ib, O, seed=1234):
     (1024, 512, 32, 6),   # b = 512 slab panels, p = 2
     (640, 128, 32, 7),    # b = 128 slab path, p = 5
     (1024, 512, 64, 8),   # ib = 64 register block solves (GESSM / SSSSM), p = 2
+    (1536, 512, 64, 9),   # NEXT-1 tile shape, p = 3: chained TSTRF / SSSSM with i > k + 1
+    (768, 384, 32, 10),   # b = 384: reference-blocked kernels (not a register-slab size)
 ])
 def test_lu_parity(n, b, ib, seed):
-    A = tilegen.normal(n, seed)
+    c = lu_certified(n, b, ib, seed)
+    A, O, OL, Op = c["A"], c["O"], c["OL"], c["Op"]
     G, GL, Gp, gi = gpu_factor("lu", A, b, ib)
-    O, OL, Op, oi = oracle_factor("lu", A, b, ib)
-    assert gi == 0 and oi == 0
+    assert gi == 0 and c["info"] == 0
     p = n // b
     # pivots bit-exact on the stored vectors (k,k) and (i>k,k)
     for k in range(p):
@@ -162,13 +159,12 @@ def test_lu_parity(n, b, ib, seed):
             o = (i + k * p) * b
             assert np.array_equal(Gp[o:o + b], Op[o:o + b]), (i, k)
     errs = tile_errors("lu", G, O, n, b)
-    Pp, _ = _lu_sigma(A, b, ib, O)
-    sig = tile_errors("lu", Pp, O, n, b)
+    tol, sig = lu_tile_tolerances(c, n, b)
     for key, e in errs.items():
-        assert e <= max(TOL, 10 * sig[key]), (key, e, sig[key])
+        assert e <= tol[key], (key, e, sig[key])
     for k in range(p):
         for i in range(k + 1, p):
-            assert rel(strip(GL, p, b, ib, i, k), strip(OL, p, b, ib, i, k)) <= max(TOL, 10 * sig[(i, k)] + 1e-12)
+            assert rel(strip(GL, p, b, ib, i, k), strip(OL, p, b, ib, i, k)) <= tol[(i, k)]
     U = oracle.lu_U(G, n, b)
     NU = oracle.lu_apply_N(G, GL, Gp, U, n, b, ib)
     ro = np.linalg.norm(A - oracle.lu_apply_N(O, OL, Op, oracle.lu_U(O, n, b), n, b, ib)) / np.linalg.norm(A)
@@ -198,10 +194,14 @@ def test_lu_b1_is_gewp():
             assert P[i, k] == (2 if sw[k, i] else 1)
 
 
-def test_lu_singular_info():
-    n, b = 128, 32
+@pytest.mark.parametrize("n,b,ib,col", [
+    (128, 32, 8, 70),      # reference-blocked kernels
+    (512, 128, 32, 70),    # register-slab GETRF / TSTRF, zero pivot in the third slab
+    (768, 256, 32, 296),   # zero column b + 40: second tile column, second slab
+])
+def test_lu_singular_info(n, b, ib, col):
     A = tilegen.normal(n, 2)
-    A[:, 70] = 0.0
-    _, _, _, gi = gpu_factor("lu", A, b, 8)
-    _, _, _, oi = oracle_factor("lu", A, b, 8)
-    assert gi == oi == 71
+    A[:, col] = 0.0
+    _, _, _, gi = gpu_factor("lu", A, b, ib)
+    _, _, _, oi = oracle_factor("lu", A, b, ib)
+    assert gi == oi == col + 1

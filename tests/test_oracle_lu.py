@@ -174,5 +174,31 @@ def test_flop_formulas():
     n = p * b
     tot = sum(oracle.kernel_flops("ssrfb", b, s) * (p - k) ** 2 for k in range(1, p + 1))
     assert abs(tot / (4 * n**3 / 3 * (1 + s / (4 * b))) - 1) < 0.01
+    tot = sum(oracle.kernel_flops("ssssm", b, s) * (p - k) ** 2 for k in range(1, p + 1))
+    assert abs(tot / (2 * n**3 / 3 * (1 + s / (2 * b))) - 1) < 0.01
+    # kinds without a printed count in the paper are not provided
+    assert np.isnan(oracle.kernel_flops("gemm", b, s)) and np.isnan(oracle.kernel_flops("larfb", b, s))
     # s = b gives the paper's 25% overhead
     assert (1 + b / (4 * b)) == 1.25
+
+
+def test_decision_recorder_pins():
+    """C5 instrumentation: the recorder does not change the arithmetic, records one
+    decision per pivot (p(p+1)/2 * b), and for p = 1 (GEPP) the first
+    decision is (max |A[:,0]|, second-largest |A[:,0]|) of the input, by brute force."""
+    n, b, ib = 96, 32, 8
+    A = tilegen.normal(n, 4)
+    F = oracle.pack(A, b)
+    Ls0, piv0, info0 = oracle.lu(F.copy(), n, b, ib)
+    Ls1, piv1, info1, dec = oracle.lu_decisions(F.copy(), n, b, ib)
+    assert np.array_equal(Ls0, Ls1) and np.array_equal(piv0, piv1) and info0 == info1 == 0
+    p = n // b
+    assert dec.shape == (p * (p + 1) // 2 * b, 2)
+    assert (dec[:, 0] >= dec[:, 1]).all()
+    A1 = tilegen.normal(32, 5)
+    _, _, _, d1 = oracle.lu_decisions(oracle.pack(A1, 32), 32, 32, 8)
+    col = np.sort(np.abs(A1[:, 0]))
+    assert d1[0, 0] == col[-1] and d1[0, 1] == col[-2]
+    # the unperturbed run against itself has an infinite-like margin; a perturbed run
+    # with the same pivots has a finite one
+    assert oracle.pivot_margin(dec, dec) >= 2.0 ** 40

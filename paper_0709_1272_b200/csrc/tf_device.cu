@@ -20,6 +20,9 @@
 
 #include <climits>
 
+// Every tile-kernel variant is its own (noinline) function with its own register
+// allocation; the persistent kernel's scheduler loop calls them (tf_kernels.cuh).
+#define TF_SPLIT_ITEMS
 #include "tf_kernels.cuh"
 #include "tf_sched.h"
 

@@ -33,6 +33,39 @@ struct Ctx {
   int* abort_flag;  // set on Cholesky failure: the scheduler stops handing out work
 };
 
+// Kernel variants (register-slab kernel at one tile size, or the reference-blocked path):
+// in the persistent build (TF_SPLIT_ITEMS) each variant is a separate function with its own
+// register allocation; elsewhere (tk_run, tools) they inline.  A variant re-declares the
+// dynamic shared memory so the shared address space stays known inside it.
+#ifdef TF_SPLIT_ITEMS
+#define TF_VARIANT __device__ __noinline__
+#else
+#define TF_VARIANT __device__ __forceinline__
+#endif
+#define TF_DSM_DECL extern __shared__ __align__(16) double dsm[]
+#define TF_DEF_VARIANT(name, fn, params, args) \
+  template <int MI>                             \
+  TF_VARIANT void name params {                 \
+    TF_DSM_DECL;                                \
+    fn<MI> args;                                \
+  }
+#define TF_DEF_VARIANT_RET(name, fn, params, args) \
+  template <int MI>                                 \
+  TF_VARIANT int name params {                      \
+    TF_DSM_DECL;                                    \
+    return fn<MI> args;                             \
+  }
+#define TF_DEF_REF(name, fn, params, args) \
+  TF_VARIANT void name params {             \
+    TF_DSM_DECL;                            \
+    fn args;                                \
+  }
+#define TF_DEF_REF_RET(name, fn, params, args) \
+  TF_VARIANT int name params {                  \
+    TF_DSM_DECL;                                \
+    return fn args;                             \
+  }
+
 using GemmNT128 = Gemm<128, 128, 4, 4, false, false>;
 using GemmNT32 = Gemm<128, 32, 8, 2, false, false>;
 using GemmW64 = Gemm<64, 64, 4, 4, true, true>;
@@ -212,9 +245,8 @@ __device__ inline int potrf_left(const Ctx& cx, double* A, double* sm) {
 // POTRF for b a multiple of 128 (>= 256): right-looking over 128-column panels — each panel
 // is factored left-looking in 32-column steps (K limited to the panel), then the trailing
 // lower triangle takes the rank-128 update as 128x128 DMMA tiles (SYRK/GEMM shape, K = 128).
-__device__ inline int potrf_item(const Ctx& cx, double* A, double* sm) {
+__device__ inline int potrf_right(const Ctx& cx, double* A, double* sm) {
   const int b = cx.b;
-  if (b < 256 || b % 128) return potrf_left(cx, A, sm);
   double* D = sm + GemmNT32::SMEM_DOUBLES;
   int* sflag = reinterpret_cast<int*>(D + (NB + 1) * NB);
   for (int J = 0; J < b; J += 128) {
@@ -281,9 +313,8 @@ __device__ inline void trsm_left(const Ctx& cx, const double* L, double* X, int 
 // TRSM for b a multiple of 128 (>= 256): right-looking over 128-column panels as POTRF —
 // each panel solved left-looking in 32-column steps (K limited to the panel), then the
 // columns to its right take the rank-128 update as 128x128 DMMA tiles (K = 128).
-__device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int item, double* sm) {
+__device__ inline void trsm_right(const Ctx& cx, const double* L, double* X, int item, double* sm) {
   const int b = cx.b;
-  if (b < 256 || b % 128) { trsm_left(cx, L, X, item, sm); return; }
   const int r0 = item * RB, rows = min(RB, b - r0);
   double* D = sm + GemmNT32::SMEM_DOUBLES;
   X += r0;
@@ -312,7 +343,7 @@ __device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int 
 }
 
 // SYRK (DGSMM with i = j): lower sub-tile `item` of C -= A A^T.
-__device__ inline void syrk_item(const Ctx& cx, const double* A, double* C, int item, double* sm) {
+__device__ inline void syrk_body(const Ctx& cx, const double* A, double* C, int item, double* sm) {
   const int b = cx.b;
   int mi = 0, rem = item;
   while (rem > mi) { rem -= mi + 1; ++mi; }
@@ -327,7 +358,7 @@ __device__ inline void syrk_item(const Ctx& cx, const double* A, double* C, int 
 }
 
 // GEMM (DGSMM with i > j): sub-tile `item` of C -= A B^T.
-__device__ inline void gemm_item(const Ctx& cx, const double* A, const double* B, double* C, int item,
+__device__ inline void gemm_body(const Ctx& cx, const double* A, const double* B, double* C, int item,
                                  double* sm) {
   const int b = cx.b;
   const int nr = ceil_div(b, RB);
@@ -377,6 +408,29 @@ __device__ inline void gemm_item(const Ctx& cx, const double* A, const double* B
   sub_store(g, C + m0 + (size_t)n0 * b, b, mm, nn);
   __syncthreads();
   TF_PROBE_MARK(2, t0);
+}
+
+TF_DEF_REF_RET(v_potrf_left, potrf_left, (Ctx cx, double* A), (cx, A, dsm))
+TF_DEF_REF_RET(v_potrf_right, potrf_right, (Ctx cx, double* A), (cx, A, dsm))
+TF_DEF_REF(v_trsm_left, trsm_left, (Ctx cx, const double* L, double* X, int item), (cx, L, X, item, dsm))
+TF_DEF_REF(v_trsm_right, trsm_right, (Ctx cx, const double* L, double* X, int item), (cx, L, X, item, dsm))
+TF_DEF_REF(v_syrk, syrk_body, (Ctx cx, const double* A, double* C, int item), (cx, A, C, item, dsm))
+TF_DEF_REF(v_gemm, gemm_body, (Ctx cx, const double* A, const double* B, double* C, int item), (cx, A, B, C, item, dsm))
+
+// Cholesky task kernels (the `sm` argument is the caller's dynamic shared memory; the
+// variants re-declare it).  POTRF / TRSM: right-looking over 128-column panels for b a
+// multiple of 128 (>= 256), left-looking 32-column blocks otherwise.
+__device__ inline int potrf_item(const Ctx& cx, double* A, double*) {
+  if (cx.b < 256 || cx.b % 128) return v_potrf_left(cx, A);
+  return v_potrf_right(cx, A);
+}
+__device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int item, double*) {
+  if (cx.b < 256 || cx.b % 128) v_trsm_left(cx, L, X, item);
+  else v_trsm_right(cx, L, X, item);
+}
+__device__ inline void syrk_item(const Ctx& cx, const double* A, double* C, int item, double*) { v_syrk(cx, A, C, item); }
+__device__ inline void gemm_item(const Ctx& cx, const double* A, const double* B, double* C, int item, double*) {
+  v_gemm(cx, A, B, C, item);
 }
 
 // ====================================================================================
@@ -657,27 +711,40 @@ namespace tf {
     else fn<1>(__VA_ARGS__);                           \
   } while (0)
 
+TF_DEF_VARIANT(v_qr_slab, qr_slab, (Ctx cx, bool ts, double* A, double* R, double* Tst, double* VX),
+               (cx, ts, A, R, Tst, VX, dsm))
+TF_DEF_VARIANT(v_larfb_reg, larfb_reg, (Ctx cx, const double* VX, const double* Tst, double* C, int item),
+               (cx, VX, Tst, C, item, dsm))
+TF_DEF_VARIANT(v_ssrfb_reg, ssrfb_reg, (Ctx cx, const double* V, const double* Tst, double* R, double* A, int item),
+               (cx, V, Tst, R, A, item, dsm))
+TF_DEF_REF(v_geqrt_ref, geqrt_ref, (Ctx cx, double* A, double* Tst, double* VX), (cx, A, Tst, VX, dsm))
+TF_DEF_REF(v_larfb_ref, larfb_ref, (Ctx cx, const double* VX, const double* Tst, double* C, int item),
+           (cx, VX, Tst, C, item, dsm))
+TF_DEF_REF(v_tsqrt_ref, tsqrt_ref, (Ctx cx, double* R, double* A, double* Tst), (cx, R, A, Tst, dsm))
+TF_DEF_REF(v_ssrfb_ref, ssrfb_ref, (Ctx cx, const double* V, const double* Tst, double* R, double* A, int item),
+           (cx, V, Tst, R, A, item, dsm))
+
 // GEQRT: A_kk -> V_kk, R_kk, T_kk; writes the unit-lower V copy VX.
 __device__ inline void geqrt_item(const Ctx& cx, double* A, double* Tst, double* VX, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(qr_slab, cx, false, A, nullptr, Tst, VX, sm);
-  else geqrt_ref(cx, A, Tst, VX, sm);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_qr_slab, cx, false, A, nullptr, Tst, VX);
+  else v_geqrt_ref(cx, A, Tst, VX);
 }
 // LARFB: slab `item` of C <- Q_kk^T C.
 __device__ inline void larfb_item(const Ctx& cx, const double* VX, const double* Tst, double* C, int item,
                                   double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(larfb_reg, cx, VX, Tst, C, item, sm);
-  else larfb_ref(cx, VX, Tst, C, item, sm);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_larfb_reg, cx, VX, Tst, C, item);
+  else v_larfb_ref(cx, VX, Tst, C, item);
 }
 // TSQRT: QR of [R_kk; A_ik]; only the upper region of R_kk is touched.
 __device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* Tst, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(qr_slab, cx, true, A, R, Tst, nullptr, sm);
-  else tsqrt_ref(cx, R, A, Tst, sm);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_qr_slab, cx, true, A, R, Tst, nullptr);
+  else v_tsqrt_ref(cx, R, A, Tst);
 }
 // SSRFB: slab `item` of [R_kj; A_ij] <- Q_ik^T [R_kj; A_ij].
 __device__ inline void ssrfb_item(const Ctx& cx, const double* V, const double* Tst, double* R, double* A,
                                   int item, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(ssrfb_reg, cx, V, Tst, R, A, item, sm);
-  else ssrfb_ref(cx, V, Tst, R, A, item, sm);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_ssrfb_reg, cx, V, Tst, R, A, item);
+  else v_ssrfb_ref(cx, V, Tst, R, A, item);
 }
 
 // ====================================================================================
@@ -993,26 +1060,42 @@ __device__ inline void ssssm_ref(const Ctx& cx, const double* L, const double* L
 #include "tf_lu_slab.cuh"
 namespace tf {
 
+TF_DEF_VARIANT(v_gessm_reg, gessm_reg, (Ctx cx, const double* LX, const int* ipiv, double* C, int item),
+               (cx, LX, ipiv, C, item, dsm))
+TF_DEF_VARIANT(v_ssssm_reg, ssssm_reg,
+               (Ctx cx, const double* L, const double* Ls, const int* ipiv, double* U, double* A, int item),
+               (cx, L, Ls, ipiv, U, A, item, dsm))
+TF_DEF_VARIANT_RET(v_getrf_slab, getrf_slab, (Ctx cx, double* A, int* ipiv, double* LX), (cx, A, ipiv, LX, dsm))
+TF_DEF_VARIANT_RET(v_tstrf_slab, tstrf_slab, (Ctx cx, double* U, double* A, double* Ls, int* ipiv),
+                   (cx, U, A, Ls, ipiv, dsm))
+TF_DEF_REF(v_gessm_ref, gessm_ref, (Ctx cx, const double* LX, const int* ipiv, double* C, int item),
+           (cx, LX, ipiv, C, item, dsm))
+TF_DEF_REF(v_ssssm_ref, ssssm_ref,
+           (Ctx cx, const double* L, const double* Ls, const int* ipiv, double* U, double* A, int item),
+           (cx, L, Ls, ipiv, U, A, item, dsm))
+TF_DEF_REF_RET(v_getrf_ref, getrf_ref, (Ctx cx, double* A, int* ipiv, double* LX), (cx, A, ipiv, LX, dsm))
+TF_DEF_REF_RET(v_tstrf_ref, tstrf_ref, (Ctx cx, double* U, double* A, double* Ls, int* ipiv), (cx, U, A, Ls, ipiv, dsm))
+
 // LU update task kernels: register-slab path for b in {128, 256, 512}, ib in {32, 64}.
 __device__ inline void gessm_item(const Ctx& cx, const double* LX, const int* ipiv, double* C, int item,
                                   double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(gessm_reg, cx, LX, ipiv, C, item, sm);
-  else gessm_ref(cx, LX, ipiv, C, item, sm);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_gessm_reg, cx, LX, ipiv, C, item);
+  else v_gessm_ref(cx, LX, ipiv, C, item);
 }
 __device__ inline void ssssm_item(const Ctx& cx, const double* L, const double* Ls, const int* ipiv, double* U,
                                   double* A, int item, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(ssssm_reg, cx, L, Ls, ipiv, U, A, item, sm);
-  else ssssm_ref(cx, L, Ls, ipiv, U, A, item, sm);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_ssssm_reg, cx, L, Ls, ipiv, U, A, item);
+  else v_ssssm_ref(cx, L, Ls, ipiv, U, A, item);
 }
-// LU panel tasks: slab kernels for ib = 32 (the slab is the inner block).
+// LU panel tasks: slab kernels for ib in {32, 64} (32-column slabs).
 #define TF_SLAB_RET(fn, ...) (cx.b == 512 ? fn<4>(__VA_ARGS__) : cx.b == 256 ? fn<2>(__VA_ARGS__) : fn<1>(__VA_ARGS__))
 __device__ inline int getrf_item(const Ctx& cx, double* A, int* ipiv, double* LX, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib) && cx.ib == 32) return TF_SLAB_RET(getrf_slab, cx, A, ipiv, LX, sm);
-  return getrf_ref(cx, A, ipiv, LX, sm);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) return TF_SLAB_RET(v_getrf_slab, cx, A, ipiv, LX);
+  return v_getrf_ref(cx, A, ipiv, LX);
 }
 __device__ inline int tstrf_item(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib) && cx.ib == 32) return TF_SLAB_RET(tstrf_slab, cx, U, A, Ls, ipiv, sm);
-  return tstrf_ref(cx, U, A, Ls, ipiv, sm);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) return TF_SLAB_RET(v_tstrf_slab, cx, U, A, Ls, ipiv);
+  return v_tstrf_ref(cx, U, A, Ls, ipiv);
 }
 
 }  // namespace tf

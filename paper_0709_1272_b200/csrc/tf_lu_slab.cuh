@@ -57,7 +57,7 @@ __device__ __forceinline__ void lu_block_solve(double* sU, const double* sL, int
 }
 
 #ifdef TF_PROF_LU
-__device__ long long g_lu_prof[16];
+__device__ long long g_lu_prof[24];  // 12-15: lu_panel phases (argmax, barrier, merge, update); 16-20: lu_ts_apply
 #define TF_LU_T0() long long lu_t_ = clock64()
 #define TF_LU_T(k)                                                       \
   do {                                                                   \
@@ -76,34 +76,66 @@ __device__ long long g_lu_prof[16];
 // [U_s; A] <- swaps of block s, U_s <- (I + Ls_s)^{-1} U_s, A -= L[:, s] U_s.
 //   Us  : U rows c0.. of the slab columns, (m, c) at Us[m + c*b] (read, then written back)
 //   Lc  : L columns of the block, (r, m) at Lc[r + m*b]
-//   Lsb : Ls block s, (r, m) at Lsb[r + m*ib];  pv: the block's ib pivots (1-based, [1, 2b])
-template <int MI>
-__device__ __forceinline__ void lu_ts_apply(double (&acc)[MI][SNJ][2], double* Us, const double* Lc, const double* Lsb,
-                                            const int* pv, int ib, int b, double* sm) {
+//   Lsb : Ls block s, (r, m) at Lsb[r + m*ldl];  pv: the block's IB pivots (1-based, [1, 2b])
+// (IB may be a 32-column sub-block of a 64-column inner block: ldl = the strip's ib)
+// The sequential pairwise swaps (top row jj <-> the bottom row pivot jj names, jj in order)
+// are composed per 32 pivots with __match_any_sync: top row jj ends with the original
+// content of the previous top row that named the same bottom row (or of that bottom row if
+// none), and a named bottom row ends with the last top row that named it.  Each column then
+// gathers in two shared-memory round trips instead of a 32-step dependent chain.
+template <int MI, int IB>
+__device__ __forceinline__ void lu_ts_apply_t(double (&acc)[MI][SNJ][2], double* Us, const double* Lc,
+                                              const double* Lsb, const int* pv, int ldl, int b, double* sm) {
   constexpr int RW = 8 * MI;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   const int r0 = warp * RW;
-  double* sU = sm;                              // ib x LU_LDW: U_s
-  double* sA = sU + 64 * LU_LDW;                // ib slots x LU_LDW: the A rows the pivots name
-  double* sL = sA + 64 * LU_LDW;                // ib x (ib+1): L(r, m), r > m
+  double* sU = sm;                              // IB x LU_LDW: U_s
+  double* sA = sU + 64 * LU_LDW;                // IB slots x LU_LDW: the A rows the pivots name
+  double* sL = sA + 64 * LU_LDW;                // IB x (IB+1): L(r, m), r > m
   int* flag = reinterpret_cast<int*>(sL + 64 * 65);  // b: slot of bottom row r (INT_MAX = none)
-  int* spv = flag + 512;                        // ib pivots of the block
+  int* spv = flag + 512;                        // IB pivots of the block
+  int* srcT = spv + 64;                         // top row P <- top row srcT (< 64) or slot srcT - 64
+  int* lastS = srcT + 64;                       // [half][slot]: the slot <- top row lastS (-1: kept)
+  // the L columns of the update, in flight from the start (they are this block's own
+  // results, L2-resident): MI * IB/4 values per thread
+  constexpr int NPRE = (MI * IB / 4 <= 16) ? IB / 4 : 0;
+  double la[NPRE > 0 ? NPRE : 1][MI];
+  TF_LU_T0();
+#pragma unroll
+  for (int ks = 0; ks < NPRE; ++ks)
+#pragma unroll
+    for (int i = 0; i < MI; ++i) la[ks][i] = -Lc[(r0 + 8 * i + g) + (size_t)(4 * ks + q) * b];
   for (int r = tid; r < b; r += TF_THREADS) flag[r] = INT_MAX;
-  for (int e = tid; e < ib * NSR; e += TF_THREADS) {
-    const int m = e % ib, c = e / ib;
+  if (tid < IB) spv[tid] = pv[tid];
+  for (int e = tid; e < IB * NSR; e += TF_THREADS) {
+    const int m = e % IB, c = e / IB;
     sU[m * LU_LDW + c] = ldg_cg(Us + m + (size_t)c * b);
   }
-  for (int e = tid; e < ib * ib; e += TF_THREADS) {
-    const int r = e % ib, m = e / ib;
-    sL[r * (ib + 1) + m] = (r > m) ? ldg_cg(Lsb + e) : 0.0;
+  for (int e = tid; e < IB * IB; e += TF_THREADS) {
+    const int r = e % IB, m = e / IB;
+    sL[r * (IB + 1) + m] = (r > m) ? ldg_cg(Lsb + r + (size_t)m * ldl) : 0.0;
   }
   __syncthreads();
-  if (tid < ib) {
-    const int v = pv[tid];
-    spv[tid] = v;
+  TF_LU_T(16);
+  if (tid < IB) {
+    const int v = spv[tid];
     if (v > b) atomicMin(&flag[v - b - 1], tid);  // slot = first pivot naming the row
   }
   __syncthreads();
+  // compose each half's swaps (warp h: pivots 32h .. 32h + 31)
+  if (warp < IB / 32) {
+    const int P = 32 * warp + lane;
+    const int v = spv[P];
+    const int f = v > b ? flag[v - b - 1] : -1;
+    const unsigned m = __match_any_sync(0xffffffffu, f >= 0 ? f : 1000 + P);
+    const unsigned below = m & ((1u << lane) - 1u);
+    const int prev = below ? 31 - __clz(below) : -1;
+    srcT[P] = f < 0 ? P : (prev >= 0 ? 32 * warp + prev : 64 + f);
+    lastS[warp * 64 + lane] = -1;
+    lastS[warp * 64 + 32 + lane] = -1;
+    __syncwarp();
+    if (f >= 0 && (m >> lane) == 1u) lastS[warp * 64 + f] = P;
+  }
   // named A rows: registers -> smem slots
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
@@ -115,22 +147,37 @@ __device__ __forceinline__ void lu_ts_apply(double (&acc)[MI][SNJ][2], double* U
         for (int e = 0; e < 2; ++e) sA[f * LU_LDW + 8 * j + 2 * q + e] = acc[i][j][e];
   }
   __syncthreads();
-  // pairwise swaps in pivot order, then the unit-lower solve (per column)
+  TF_LU_T(17);
+  // the composed swaps (16 lanes per column), then the unit-lower solve (per column)
   {
-    const int c = tid >> 4;
-    if ((tid & 15) == 0)
-      for (int jj = 0; jj < ib; ++jj) {
-        const int v = spv[jj];
-        if (v > b) {
-          const int f = flag[v - b - 1];
-          const double t = sU[jj * LU_LDW + c];
-          sU[jj * LU_LDW + c] = sA[f * LU_LDW + c];
-          sA[f * LU_LDW + c] = t;
-        }
+    const int c = tid >> 4, l = tid & 15;
+#pragma unroll
+    for (int h = 0; h < IB / 32; ++h) {
+      double vt[2], vs[IB / 16];
+      int ls[IB / 16];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int sr = srcT[32 * h + l + 16 * u];
+        vt[u] = sr < 64 ? sU[sr * LU_LDW + c] : sA[(sr - 64) * LU_LDW + c];
       }
-    lu_block_solve(sU, sL, ib);
+#pragma unroll
+      for (int u = 0; u < IB / 16; ++u) {
+        const int f = l + 16 * u;
+        ls[u] = lastS[h * 64 + f];
+        vs[u] = ls[u] >= 0 ? sU[ls[u] * LU_LDW + c] : 0.0;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 2; ++u) sU[(32 * h + l + 16 * u) * LU_LDW + c] = vt[u];
+#pragma unroll
+      for (int u = 0; u < IB / 16; ++u)
+        if (ls[u] >= 0) sA[(l + 16 * u) * LU_LDW + c] = vs[u];
+      __syncwarp();
+    }
+    lu_block_solve(sU, sL, IB);
   }
   __syncthreads();
+  TF_LU_T(18);
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
     const int f = flag[r0 + 8 * i + g];
@@ -140,15 +187,17 @@ __device__ __forceinline__ void lu_ts_apply(double (&acc)[MI][SNJ][2], double* U
 #pragma unroll
         for (int e = 0; e < 2; ++e) acc[i][j][e] = sA[f * LU_LDW + 8 * j + 2 * q + e];
   }
-  for (int e = tid; e < ib * NSR; e += TF_THREADS) {
-    const int m = e % ib, c = e / ib;
+  for (int e = tid; e < IB * NSR; e += TF_THREADS) {
+    const int m = e % IB, c = e / IB;
     Us[m + (size_t)c * b] = sU[m * LU_LDW + c];
   }
+  TF_LU_T(19);
   // A -= L[:, block] U_s
-  for (int ks = 0; ks < ib / 4; ++ks) {
+#pragma unroll
+  for (int ks = 0; ks < IB / 4; ++ks) {
     double a[MI], bq[SNJ];
 #pragma unroll
-    for (int i = 0; i < MI; ++i) a[i] = -Lc[(r0 + 8 * i + g) + (size_t)(4 * ks + q) * b];
+    for (int i = 0; i < MI; ++i) a[i] = NPRE ? la[NPRE ? ks : 0][i] : -Lc[(r0 + 8 * i + g) + (size_t)(4 * ks + q) * b];
 #pragma unroll
     for (int j = 0; j < SNJ; ++j) bq[j] = sU[(4 * ks + q) * LU_LDW + 8 * j + g];
 #pragma unroll
@@ -157,6 +206,14 @@ __device__ __forceinline__ void lu_ts_apply(double (&acc)[MI][SNJ][2], double* U
       for (int j = 0; j < SNJ; ++j) dmma(acc[i][j], a[i], bq[j]);
   }
   __syncthreads();
+  TF_LU_T(20);
+}
+
+template <int MI>
+__device__ __forceinline__ void lu_ts_apply(double (&acc)[MI][SNJ][2], double* Us, const double* Lc, const double* Lsb,
+                                            const int* pv, int ib, int ldl, int b, double* sm) {
+  if (ib == 32) lu_ts_apply_t<MI, 32>(acc, Us, Lc, Lsb, pv, ldl, b, sm);
+  else lu_ts_apply_t<MI, 64>(acc, Us, Lc, Lsb, pv, ldl, b, sm);
 }
 
 // SSSSM item: 32 columns of [U_kj; A_ij].  L = A_ik (multipliers), Ls = L strip (i,k),
@@ -170,7 +227,7 @@ __device__ inline void ssssm_reg(const Ctx& cx, const double* L, const double* L
   double acc[MI][SNJ][2];
   slab_load<MI>(acc, A, b);
   for (int c0 = 0; c0 < b; c0 += ib)
-    lu_ts_apply<MI>(acc, U + c0, L + (size_t)c0 * b, Ls + (size_t)c0 * ib, ipiv + c0, ib, b, sm);
+    lu_ts_apply<MI>(acc, U + c0, L + (size_t)c0 * b, Ls + (size_t)c0 * ib, ipiv + c0, ib, ib, b, sm);
   slab_store<MI>(acc, A, b);
 }
 
@@ -217,18 +274,34 @@ __device__ __forceinline__ void lu_rows_permute(double (&acc)[MI][SNJ][2], const
   __syncthreads();
 }
 
-// Block [c0, c0+ib) of the unit-lower solve on the register slab: its rows <- L_ss^{-1} rows
-// (forward substitution), rows below -= L[rows, c0:c0+ib] * block rows (DMMA).  Lt: the tile
+// Block [c0, c0+IB) of the unit-lower solve on the register slab: its rows <- L_ss^{-1} rows
+// (forward substitution), rows below -= L[rows, c0:c0+IB] * block rows (DMMA).  Lt: the tile
 // holding L (explicit unit-lower copy or the factored tile itself; only r > c is read).
-template <int MI>
-__device__ __forceinline__ void lu_rows_block(double (&acc)[MI][SNJ][2], const double* Lt, int c0, int ib, int b,
-                                              double* sm) {
+// The update's L operand is loaded at the start (in flight during the solve) when it fits.
+#ifndef TF_RB_PRE
+#define TF_RB_PRE 8
+#endif
+template <int MI, int IB>
+__device__ __forceinline__ void lu_rows_block_t(double (&acc)[MI][SNJ][2], const double* Lt, int c0, int b,
+                                                double* sm) {
   constexpr int RW = 8 * MI;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   const int r0 = warp * RW;
-  const int c1 = c0 + ib;
-  double* sU = sm;                // ib x LU_LDW
-  double* sL = sU + 64 * LU_LDW;  // ib x (ib+1)
+  const int c1 = c0 + IB;
+  double* sU = sm;                // IB x LU_LDW
+  double* sL = sU + 64 * LU_LDW;  // IB x (IB+1)
+  const bool upd = c1 < b && r0 + RW > c1;
+  constexpr int NPRE = (MI * IB / 4 <= TF_RB_PRE) ? IB / 4 : 0;
+  double la[NPRE > 0 ? NPRE : 1][MI];
+  if (upd) {
+#pragma unroll
+    for (int ks = 0; ks < NPRE; ++ks)
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        const int row = r0 + 8 * i + g;
+        la[ks][i] = row >= c1 ? -Lt[row + (size_t)(c0 + 4 * ks + q) * b] : 0.0;
+      }
+  }
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
     const int row = r0 + 8 * i + g;
@@ -238,12 +311,12 @@ __device__ __forceinline__ void lu_rows_block(double (&acc)[MI][SNJ][2], const d
 #pragma unroll
         for (int e = 0; e < 2; ++e) sU[(row - c0) * LU_LDW + 8 * j + 2 * q + e] = acc[i][j][e];
   }
-  for (int e = tid; e < ib * ib; e += TF_THREADS) {
-    const int r = e % ib, m = e / ib;
-    sL[r * (ib + 1) + m] = (r > m) ? ldg_cg(Lt + (c0 + r) + (size_t)(c0 + m) * b) : 0.0;
+  for (int e = tid; e < IB * IB; e += TF_THREADS) {
+    const int r = e % IB, m = e / IB;
+    sL[r * (IB + 1) + m] = (r > m) ? ldg_cg(Lt + (c0 + r) + (size_t)(c0 + m) * b) : 0.0;
   }
   __syncthreads();
-  lu_block_solve(sU, sL, ib);
+  lu_block_solve(sU, sL, IB);
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
@@ -254,13 +327,14 @@ __device__ __forceinline__ void lu_rows_block(double (&acc)[MI][SNJ][2], const d
 #pragma unroll
         for (int e = 0; e < 2; ++e) acc[i][j][e] = sU[(row - c0) * LU_LDW + 8 * j + 2 * q + e];
   }
-  if (c1 < b && r0 + RW > c1) {
-    for (int ks = 0; ks < ib / 4; ++ks) {
+  if (upd) {
+#pragma unroll
+    for (int ks = 0; ks < IB / 4; ++ks) {
       double a[MI], bq[SNJ];
 #pragma unroll
       for (int i = 0; i < MI; ++i) {
         const int row = r0 + 8 * i + g;
-        a[i] = row >= c1 ? -Lt[row + (size_t)(c0 + 4 * ks + q) * b] : 0.0;
+        a[i] = NPRE ? la[NPRE ? ks : 0][i] : (row >= c1 ? -Lt[row + (size_t)(c0 + 4 * ks + q) * b] : 0.0);
       }
 #pragma unroll
       for (int j = 0; j < SNJ; ++j) bq[j] = sU[(4 * ks + q) * LU_LDW + 8 * j + g];
@@ -271,6 +345,13 @@ __device__ __forceinline__ void lu_rows_block(double (&acc)[MI][SNJ][2], const d
     }
   }
   __syncthreads();
+}
+
+template <int MI>
+__device__ __forceinline__ void lu_rows_block(double (&acc)[MI][SNJ][2], const double* Lt, int c0, int ib, int b,
+                                              double* sm) {
+  if (ib == 32) lu_rows_block_t<MI, 32>(acc, Lt, c0, b, sm);
+  else lu_rows_block_t<MI, 64>(acc, Lt, c0, b, sm);
 }
 
 // GESSM item: 32 columns of C = A_kj <- L_kk^{-1} P_kk C.  LX = explicit unit-lower L_kk
@@ -288,7 +369,9 @@ __device__ inline void gessm_reg(const Ctx& cx, const double* LX, const int* ipi
 }
 
 // LU panel of one 32-column slab held as P (smem, b x 32, column-major, ld ldp) on entry and
-// exit; registers during the factorization (warp w: rows [w*RW, (w+1)*RW), lane c: column c).
+// exit.  Row-per-thread during the factorization: thread t < b keeps row t of the slab (32
+// doubles) in registers, so the pivot search of a column is a reduction over threads and
+// the rank-1 update is 31 - jj FMAs per thread with the pivot row broadcast from smem.
 //   TS (TSTRF): pairwise pivoting of column jj between the top row jj of
 //       UL (32 x 33: U of the slab's diagonal block above the diagonal, the L-strip block
 //       below it, footnote PAPER.md:542-544) and all b rows of P; the top row wins ties
@@ -297,143 +380,130 @@ __device__ inline void gessm_reg(const Ctx& cx, const double* LX, const int* ipi
 //   !TS (GETRF): partial pivoting over tile rows >= cs + jj of P (first
 //       maximum), rows swapped over the slab's 32 columns (the caller applies them to the
 //       other columns, Z12); pivots cs-relative rows + 1 in [1, b].
-// Column jj: lane jj's local argmax -> barrier -> every warp merges in warp order -> the
-// rows involved in the swap are published -> barrier -> swap, scaling by the pivot
-// (division, as the oracle), rank-1 update of columns > jj.  Returns the first zero-pivot
-// local column or -1.
+// Column jj, ONE CTA barrier: every warp reduces its 32 rows to (max |x|, first row) with
+// three redux.sync (max of the high word, max of the low word among those, min row among
+// those: |x| >= 0 orders like its bit pattern) and its winning lane publishes the whole
+// candidate row (GETRF also publishes row cs + jj) into parity-double-buffered smem;
+// after the barrier every warp merges the 16 warp candidates the same way, so all threads
+// know the pivot row and read its values from the winner's published copy.  The swap, the
+// division by the pivot (division, as the oracle) and the update follow without another
+// barrier.  Returns the first zero-pivot local column or -1.
+__device__ __forceinline__ void warp_first_max(double v, int idx, double& bv, int& bi) {
+  // v >= 0 (fabs), idx = row (INT_MAX: no candidate).  Largest v, then smallest idx.
+  const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  bi = __reduce_min_sync(0xffffffffu, (hi == mhi && lo == mlo) ? idx : INT_MAX);
+  bv = __hiloint2double((int)mhi, (int)mlo);
+}
+
 template <int MI, bool TS>
 __device__ inline int lu_panel(double* P, int ldp, int cs, int b, double* UL, int* piv, double* sm2) {
-  constexpr int RW = 8 * MI;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int c = lane, r0w = warp * RW;
-  double* amv = sm2;                                     // 16 warp maxima
-  int* ami = reinterpret_cast<int*>(amv + 16);           // 16 warp argmax rows
-  double* rowA = amv + 32;                               // 32: pivot row (pre-swap)
-  double* rowB = rowA + 32;                              // 32: GETRF row cs + jj (pre-swap)
-  double* xcol = rowB + 32;                              // 16 x RW: scaled column jj per warp
-  double* xw = xcol + warp * RW;
-  double p[RW];
+  const int nwa = (b + 31) >> 5;                         // warps that own rows
+  const bool own = tid < b;
+  double* cval = sm2;                                    // 2 x 16 warp maxima
+  int* cidx = reinterpret_cast<int*>(sm2 + 32);          // 2 x 16 warp argmax rows
+  double* crow = sm2 + 64;                               // 2 x 16 x 32 candidate rows
+  double* trow = crow + 2 * 16 * 32;                     // 2 x 32: GETRF row cs + jj (pre-swap)
+  double x[32];
 #pragma unroll
-  for (int k = 0; k < RW; ++k) p[k] = P[(r0w + k) + (size_t)c * ldp];
+  for (int c = 0; c < 32; ++c) x[c] = own ? P[tid + (size_t)c * ldp] : 0.0;
   int first_zero = -1;
+  TF_LU_T0();
+#pragma unroll
   for (int jj = 0; jj < 32; ++jj) {
+    const int par = jj & 1;
     const int cg = cs + jj;
-    const int kcg = cg - r0w;
-    // lane jj: first maximum of |x| over this warp's candidate rows
-    // (pairwise trees over ordered halves: the left operand holds the lower rows, so taking
-    //  the right one only when strictly larger keeps the first maximum)
-    if (c == jj) {
-      double v[RW];
-      int id[RW];
-#pragma unroll
-      for (int k = 0; k < RW; ++k) {
-        v[k] = (TS || k >= kcg) ? fabs(p[k]) : -1.0;
-        id[k] = (TS || k >= kcg) ? r0w + k : INT_MAX;
+    // (TSTRF) the top candidate is read before the barrier: the winner rewrites UL row jj
+    // after it, while slower warps may still be comparing
+    const double top = TS ? fabs(UL[jj * 33 + jj]) : 0.0;
+    if (warp < nwa) {
+      const bool cand = own && (TS || tid >= cg);
+      double wv;
+      int wi;
+      warp_first_max(cand ? fabs(x[jj]) : 0.0, cand ? tid : INT_MAX, wv, wi);
+      if (lane == 0) {
+        cval[par * 16 + warp] = wv;
+        cidx[par * 16 + warp] = wi;
       }
+      if (tid == wi) {
+        double2* d = reinterpret_cast<double2*>(crow + (par * 16 + warp) * 32);
 #pragma unroll
-      for (int st = 1; st < RW; st *= 2)
+        for (int c = 0; c < 32; c += 2) d[c >> 1] = make_double2(x[c], x[c + 1]);
+      }
+      if (!TS && tid == cg) {
+        double2* d = reinterpret_cast<double2*>(trow + par * 32);
 #pragma unroll
-        for (int k = 0; k < RW; k += 2 * st)
-          if (v[k + st] > v[k]) { v[k] = v[k + st]; id[k] = id[k + st]; }
-      amv[warp] = v[0];
-      ami[warp] = id[0];
+        for (int c = 0; c < 32; c += 2) d[c >> 1] = make_double2(x[c], x[c + 1]);
+      }
     }
+    TF_LU_T(12);
     __syncthreads();
-    int pr;
-    {
-      double v[TF_WARPS];
-      int id[TF_WARPS];
-#pragma unroll
-      for (int w = 0; w < TF_WARPS; ++w) { v[w] = amv[w]; id[w] = ami[w]; }
-#pragma unroll
-      for (int st = 1; st < TF_WARPS; st *= 2)
-#pragma unroll
-        for (int w = 0; w < TF_WARPS; w += 2 * st)
-          if (v[w + st] > v[w]) { v[w] = v[w + st]; id[w] = id[w + st]; }
-      double bv = TS ? fabs(UL[jj * 33 + jj]) : -1.0;
-      pr = TS ? -1 : INT_MAX;
-      if (v[0] > bv) { bv = v[0]; pr = id[0]; }
-    }
-    if (!TS && pr == INT_MAX) pr = cg;  // (no candidates cannot happen: row cg itself)
-    const int kpr = pr - r0w;
-    // publish the rows the swap exchanges (pre-swap values)
-    if (pr >= 0 && kpr >= 0 && kpr < RW) {
-      double tv = 0.0;
-#pragma unroll
-      for (int k = 0; k < RW; ++k)
-        if (k == kpr) tv = p[k];
-      rowA[c] = tv;
-    }
-    if (!TS && kcg >= 0 && kcg < RW) {
-      double tv = 0.0;
-#pragma unroll
-      for (int k = 0; k < RW; ++k)
-        if (k == kcg) tv = p[k];
-      rowB[c] = tv;
-    }
-    __syncthreads();
-    // the new top / pivot row, and the swap
-    const double oldtop = TS ? UL[jj * 33 + c] : rowB[c];
-    const double newtop = (TS && pr < 0) ? oldtop : rowA[c];
-    const double u = __shfl_sync(0xffffffffu, newtop, jj);
+    TF_LU_T(13);
+    if (warp >= nwa) continue;
+    // the winner over the warp candidates (lane w holds warp w's), first maximum
+    double bv;
+    int bi;
+    warp_first_max(lane < nwa ? cval[par * 16 + lane] : 0.0, lane < nwa ? cidx[par * 16 + lane] : INT_MAX, bv, bi);
+    int pr = bi;                                         // winning row (GETRF: row >= cg exists)
+    if (TS && !(bv > top)) pr = -1;                      // the top row wins ties
+    const double* u = (!TS || pr >= 0) ? crow + (par * 16 + (pr >> 5)) * 32 : UL + jj * 33;  // the pivot row
     if (TS) {
-      if (pr >= 0 && kpr >= 0 && kpr < RW) {
+      if (pr >= 0 && tid == pr) {  // row pr <-> top row jj (the whole 32-entry row)
 #pragma unroll
-        for (int k = 0; k < RW; ++k)
-          if (k == kpr) p[k] = oldtop;
+        for (int c = 0; c < 32; ++c) {
+          const double t = UL[jj * 33 + c];
+          UL[jj * 33 + c] = x[c];
+          x[c] = t;
+        }
       }
     } else if (pr != cg) {
-      if (kpr >= 0 && kpr < RW) {
+      if (tid == cg) {
 #pragma unroll
-        for (int k = 0; k < RW; ++k)
-          if (k == kpr) p[k] = oldtop;  // row pr <- row cg
-      }
-      if (kcg >= 0 && kcg < RW) {
+        for (int c = 0; c < 32; ++c) x[c] = u[c];
+      } else if (tid == pr) {
 #pragma unroll
-        for (int k = 0; k < RW; ++k)
-          if (k == kcg) p[k] = newtop;  // row cg <- row pr
+        for (int c = 0; c < 32; ++c) x[c] = trow[par * 32 + c];
       }
     }
-    if (warp == 0) {
-      if (TS) UL[jj * 33 + c] = newtop;
-      if (c == 0) piv[jj] = TS ? (pr >= 0 ? b + pr + 1 : cg + 1) : pr + 1;
-    }
-    if (u != 0.0) {
-      // multipliers of column jj (rows below the pivot), then the rank-1 update
-      // (the divisions run one per lane, not serially on lane jj)
-      __syncwarp();
-      if (c == jj) {
+    if (tid == 0) piv[jj] = TS ? (pr >= 0 ? b + pr + 1 : cg + 1) : pr + 1;
+    TF_LU_T(14);
+    const double upiv = u[jj];
+    if (upiv != 0.0) {
+      if (own && (TS || tid > cg)) {
+        const double l = x[jj] / upiv;
+        x[jj] = l;
 #pragma unroll
-        for (int k = 0; k < RW; ++k) xw[k] = (TS || k > kcg) ? p[k] : 0.0;
-      }
-      __syncwarp();
-      if (c < RW) xw[c] = xw[c] / u;
-      __syncwarp();
-      if (c == jj) {
-#pragma unroll
-        for (int k = 0; k < RW; ++k)
-          if (TS || k > kcg) p[k] = xw[k];
-      }
-      if (c > jj) {
-#pragma unroll
-        for (int k = 0; k < RW; k += 2) {
-          const double2 x2 = *reinterpret_cast<const double2*>(xw + k);
-          p[k] = fma(-x2.x, newtop, p[k]);
-          p[k + 1] = fma(-x2.y, newtop, p[k + 1]);
-        }
+        for (int c = jj + 1; c < 32; ++c) x[c] = fma(-l, u[c], x[c]);
       }
     } else if (first_zero < 0) {
       first_zero = jj;
     }
+    TF_LU_T(15);
   }
+  if (own) {
 #pragma unroll
-  for (int k = 0; k < RW; ++k) P[(r0w + k) + (size_t)c * ldp] = p[k];
+    for (int c = 0; c < 32; ++c) P[tid + (size_t)c * ldp] = x[c];
+  }
+  // warps without rows skipped the pivot tests: every thread takes thread 0's first_zero
+  int* fz = cidx + 32;
+  if (tid == 0) *fz = first_zero;
+  __syncthreads();
+  first_zero = *fz;
   __syncthreads();
   return first_zero;
 }
 
-// TSTRF for ib = 32, left-looking over 32-column slabs: every finished
-// block's pairwise swaps / unit-lower solve / update (lu_ts_apply), then the slab's panel.
+
+// TSTRF for ib in {32, 64}, left-looking over 32-column slabs: every
+// finished inner block's pairwise swaps / unit-lower solve / update (lu_ts_apply), then the
+// slab's panel.  With ib = 64 an inner block is two slabs: the second slab first applies
+// the first slab as a 32-column sub-block (swaps of its pivots, (I + Ls_11)^{-1} on its top
+// rows, the rank-32 update), and after its own panel moves the first slab's multipliers of
+// the rows it swapped in into the L strip (footnote PAPER.md:542-544: a pivot of column j
+// exchanges the Ls row j - c0 with the bottom row over columns [c0, j); deferred to after
+// the panel, in pivot order, since nothing else touches those columns meanwhile).
 // U: the diagonal tile (upper region only is touched), A: the tile below, Ls: L strip,
 // ipiv: pivots (i,k).  Returns the first zero-pivot local column or -1.
 template <int MI>
@@ -447,9 +517,14 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
   double acc[MI][SNJ][2];
   TF_LU_T0();
   for (int cs = 0; cs < b; cs += NSR) {
+    const int s0 = cs - cs % ib, off = cs - s0;  // this slab's inner block and its offset in it
     slab_load<MI>(acc, A + (size_t)cs * b, b);
-    for (int c0 = 0; c0 < cs; c0 += ib)
-      lu_ts_apply<MI>(acc, U + c0 + (size_t)cs * b, A + (size_t)c0 * b, Ls + (size_t)c0 * ib, ipiv + c0, ib, b, sm);
+    for (int c0 = 0; c0 < s0; c0 += ib)
+      lu_ts_apply<MI>(acc, U + c0 + (size_t)cs * b, A + (size_t)c0 * b, Ls + (size_t)c0 * ib, ipiv + c0, ib, ib, b,
+                      sm);
+    if (off)  // the block's first slab, as a 32-column sub-block
+      lu_ts_apply<MI>(acc, U + s0 + (size_t)cs * b, A + (size_t)s0 * b, Ls + (size_t)s0 * ib, ipiv + s0, NSR, ib, b,
+                      sm);
     TF_LU_T(8);
     double* P = sm;
     double* UL = P + 32 * ldp;
@@ -476,7 +551,24 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
     for (int e = tid; e < 32 * 32; e += TF_THREADS) {
       const int rr = e % 32, cc = e / 32;
       if (rr <= cc) U[(cs + rr) + (size_t)(cs + cc) * b] = UL[rr * 33 + cc];
-      Ls[(size_t)(cs + cc) * ib + rr] = rr > cc ? UL[rr * 33 + cc] : 0.0;
+      Ls[(size_t)(cs + cc) * ib + off + rr] = rr > cc ? UL[rr * 33 + cc] : 0.0;
+      if (ib == 2 * NSR) Ls[(size_t)(cs + cc) * ib + (NSR - off) + rr] = 0.0;  // the other half's rows
+    }
+    __syncthreads();
+    if (off && tid < NSR) {
+      // first slab's multiplier rows swapped in by this slab's pivots -> L-strip rows
+      // (one thread per column s0 + tid, pivots in order)
+      const int c = s0 + tid;
+      for (int jj = 0; jj < NSR; ++jj) {
+        const int pv = ipiv[cs + jj];
+        if (pv > b) {
+          double* lp = Ls + (size_t)c * ib + off + jj;
+          double* ap = A + (pv - b - 1) + (size_t)c * b;
+          const double t = *lp;
+          *lp = *ap;
+          *ap = t;
+        }
+      }
     }
     __syncthreads();
     TF_LU_T(11);
@@ -484,7 +576,7 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
   return first_zero;
 }
 
-// GETRF for ib = 32, left-looking over 32-column slabs: the slab gets all
+// GETRF for ib in {32, 64}, left-looking over 32-column slabs: the slab gets all
 // earlier row interchanges and block solves/updates, then its panel; the slab's interchanges
 // are then applied to the columns on its left (LAPACK dgetrf semantics, Z12).  LX: explicit
 // unit-lower copy written at the end.  Returns the first zero-pivot local column or -1.
@@ -504,7 +596,9 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
     if (cs > 0) {
       lu_rows_permute<MI>(acc, ipiv, 0, cs, b, sm, tp);
       TF_LU_T(0);
-      for (int c0 = 0; c0 < cs; c0 += ib) lu_rows_block<MI>(acc, A, c0, ib, b, sm);
+      // unit-lower block solves / updates by 32-column blocks whatever ib is (the blocking
+      // of the forward substitution does not change it beyond rounding)
+      for (int c0 = 0; c0 < cs; c0 += NSR) lu_rows_block<MI>(acc, A, c0, NSR, b, sm);
       TF_LU_T(1);
     }
     double* P = sm;

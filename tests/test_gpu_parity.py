@@ -146,6 +146,8 @@ def test_qr_exact_pins(n, b, ib):
     (1024, 512, 64, 8),   # ib = 64 register block solves (GESSM / SSSSM), p = 2
     (1536, 512, 64, 9),   # NEXT-1 tile shape, p = 3: chained TSTRF / SSSSM with i > k + 1
     (768, 384, 32, 10),   # b = 384: reference-blocked kernels (not a register-slab size)
+    (768, 256, 64, 11),   # ib = 64 slab GETRF / TSTRF (two slabs per inner block), b = 256
+    (512, 128, 64, 12),   # ib = 64, b = 128
 ])
 def test_lu_parity(n, b, ib, seed):
     c = lu_certified(n, b, ib, seed)
@@ -172,7 +174,8 @@ def test_lu_parity(n, b, ib, seed):
 
 
 @pytest.mark.parametrize("n,b,ib", [(256, 64, 16), (96, 32, 8), (128, 128, 32),
-                                    (384, 128, 32), (512, 256, 32), (512, 512, 64)])  # register-slab sizes
+                                    (384, 128, 32), (512, 256, 32), (512, 512, 64),  # register-slab sizes
+                                    (768, 256, 64), (1024, 512, 64)])  # ib = 64 slab GETRF / TSTRF
 def test_lu_exact_pin_bitwise(n, b, ib):
     A, L0, U0 = tilegen.lu_exact(n, 3)
     G, GL, Gp, gi = gpu_factor("lu", A, b, ib)

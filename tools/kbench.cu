@@ -8,6 +8,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <vector>
+// the same noinline per-variant functions as the persistent kernel (TF_SPLIT_ITEMS), so the
+// measured code is the code the scheduler runs
+#define TF_SPLIT_ITEMS
 #include "../paper_0709_1272_b200/csrc/tf_kernels.cuh"
 
 using namespace tf;
@@ -30,19 +33,47 @@ kb_kernel(int kind, int b, int ib, double* tiles, double* aux, int* ipiv, double
   for (int r = 0; r < reps; ++r) {
     const int it = (blockIdx.x + r) % nit;
     if (threadIdx.x == 0) fence_proxy_async_all();
+#ifdef KB_KIND
+    // single-kind build (nvcc -DKB_KIND=<id>): compiles in a fraction of the time
+    if (kind != KB_KIND) continue;
+#endif
     switch (kind) {
+#if !defined(KB_KIND) || KB_KIND == 0
       case 0: potrf_item(cx, t0, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 1
       case 1: trsm_item(cx, t0, t1, it, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 2
       case 2: syrk_item(cx, t0, t1, it, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 3
       case 3: gemm_item(cx, t0, t1, t2, it, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 4
       case 4: geqrt_item(cx, t0, ax, t2, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 5
       case 5: larfb_item(cx, t0, ax, t1, it, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 6
       case 6: tsqrt_item(cx, t0, t1, ax, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 7
       case 7: ssrfb_item(cx, t0, ax, t1, t2, it, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 8
       case 8: getrf_item(cx, t0, pv, t2, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 9
       case 9: gessm_item(cx, t0, pv, t1, it, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 10
       case 10: tstrf_item(cx, t0, t1, ax, pv, sm); break;
+#endif
+#if !defined(KB_KIND) || KB_KIND == 11
       case 11: ssssm_item(cx, t0, ax, pv, t1, t2, it, sm); break;
+#endif
     }
     __syncthreads();
   }
@@ -107,13 +138,13 @@ int main(int argc, char** argv) {
 #endif
 #ifdef TF_PROF_LU
   {
-    long long z[16] = {0}, h[16];
+    long long z[24] = {0}, h[24];
     cudaMemcpyToSymbol(g_lu_prof, z, sizeof(z));
     kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps);
     CK(cudaDeviceSynchronize());
     cudaMemcpyFromSymbol(h, g_lu_prof, sizeof(h));
     printf("lu phases us/task:");
-    for (int i = 0; i < 12; ++i) if (h[i]) printf(" [%d] %.1f", i, h[i] / 1.92e3 / grid / reps);
+    for (int i = 0; i < 24; ++i) if (h[i]) printf(" [%d] %.1f", i, h[i] / 1.92e3 / grid / reps);
     printf("\n");
   }
 #endif

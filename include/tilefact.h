@@ -79,6 +79,35 @@ int tile_qr(int64_t n, int64_t b, int64_t ib, double* dA, double* dT, tf_stream_
 int tile_lu(int64_t n, int64_t b, int64_t ib, double* dA, double* dLs, int32_t* dIpiv,
             int32_t* d_info, tf_stream_t stream);
 
+/* Tiled LU without pivoting — GENP, the comparison strategy of the stability study
+ * (PAPER.md:865-873): Algorithm 3 with every pivot kept (GETRF keeps row j, TSTRF keeps
+ * the top row), so dIpiv receives the identity encodings j+1.  Same arguments, layout and
+ * info semantics as tile_lu; unstable in general (no pivoting), meant for the GETWP lab. */
+int tile_lu_nopiv(int64_t n, int64_t b, int64_t ib, double* dA, double* dLs, int32_t* dIpiv,
+                  int32_t* d_info, tf_stream_t stream);
+
+/* Solves and applies with the tiled factors.
+ * X: device, dense column-major n x nrhs with leading dimension ldx >= n, overwritten in
+ * place (internally packed into library BDL scratch with ceil(nrhs/b) tile columns; the
+ * solve runs as a DAG on the same persistent scheduler as the factorizations, reusing the
+ * factorization's update kernels on the right-hand-side tiles).  dF / dT / dLs / dIpiv are
+ * the (unmodified) outputs of tile_qr / tile_lu / tile_lu_nopiv with the same n, b, ib.
+ * Returns 0 or -k (argument k invalid) / TF_ERR_*; no numerical checks (a zero pivot gives
+ * inf / nan in X, as LAPACK getrs).  Async on `stream`.
+ *   tile_getrs      X <- A^{-1} X = U^{-1} N^{-1} X   (Eq. eq:GETWPcompact, N U = A)
+ *   tile_ormqr      X <- Q^T X                        (Algorithm 2's updates applied to X)
+ *   tile_qrs        X <- A^{-1} X = R^{-1} Q^T X
+ *   tile_lu_apply_N X <- N X  (N of Eq. eq:formula N: every elimination
+ *                   step undone in reverse order; N applied to I gives N explicitly) */
+int tile_getrs(int64_t n, int64_t b, int64_t ib, const double* dF, const double* dLs, const int32_t* dIpiv,
+               int64_t nrhs, double* dX, int64_t ldx, tf_stream_t stream);
+int tile_ormqr(int64_t n, int64_t b, int64_t ib, const double* dF, const double* dT, int64_t nrhs, double* dX,
+               int64_t ldx, tf_stream_t stream);
+int tile_qrs(int64_t n, int64_t b, int64_t ib, const double* dF, const double* dT, int64_t nrhs, double* dX,
+             int64_t ldx, tf_stream_t stream);
+int tile_lu_apply_N(int64_t n, int64_t b, int64_t ib, const double* dF, const double* dLs,
+                    const int32_t* dIpiv, int64_t nrhs, double* dX, int64_t ldx, tf_stream_t stream);
+
 size_t tile_qr_t_elems(int64_t n, int64_t b, int64_t ib);  /* p*p*ib*b */
 size_t tile_lu_l_elems(int64_t n, int64_t b, int64_t ib);  /* p*p*ib*b */
 size_t tile_lu_ipiv_elems(int64_t n, int64_t b);           /* p*p*b */
@@ -109,7 +138,8 @@ int64_t tile_trace_fetch(int64_t* rec, int64_t cap);
 void tile_set_ctas(int ctas);
 
 /* Task graph export for tests / tools (host only; no device needed).  alg: 0 chol,
- * 1 qr, 2 lu.  Returns the task count; fills up to `cap` entries of kind/k/i/j/level
+ * 1 qr, 2 lu; 3 getrs, 4 ormqr, 5 qrs, 6 lu_apply_N (solve DAGs with one X tile column;
+ * kinds 14-22 as in tf_sched.h).  Returns the task count; fills up to `cap` entries of kind/k/i/j/level
  * (kind ids: 0 POTRF 1 TRSM 2 SYRK 3 GEMM 4 GEQRT 5 LARFB 6 TSQRT 7 SSRFB 8 GETRF
  * 9 GESSM 10 TSTRF 11 SSSSM) and the CSR successor lists (succ_off has ntasks+1
  * entries; returns edge count through *nedges).  Any output pointer may be NULL. */

@@ -72,6 +72,10 @@ def lib():
             "o_chol_residual": (ctypes.c_double, [i64, dp, dp]),
             "o_kernel_flops": (ctypes.c_double, [ctypes.c_int, ctypes.c_double, ctypes.c_double]),
             "o_decisions_arm": (None, [dp, i64]),
+            "o_lu_nopiv": (ctypes.c_int, [i64, i64, i64, dp, dp, ip]),
+            "o_ref_genp": (ctypes.c_int, [i64, dp]),
+            "o_trsm_upper_bdl": (None, [i64, i64, dp, dp, i64, i64]),
+            "o_lu_solve": (None, [i64, i64, i64, dp, dp, ip, dp, i64, i64]),
             "o_decisions_count": (i64, []),
         }
         for name, (res, args) in sig.items():
@@ -193,6 +197,47 @@ def lu(tiles: np.ndarray, n: int, b: int, ib: int):
     piv = np.zeros(p * p * b, dtype=np.int32)
     info = lib().o_lu(n, b, ib, _d(tiles), _d(Ls), _i(piv))
     return Ls, piv, info
+
+
+def lu_nopiv(tiles: np.ndarray, n: int, b: int, ib: int):
+    """GENP in tiled form (Algorithm 3 with every pivot kept)."""
+    p = n // b
+    Ls = np.zeros(p * p * ib * b, dtype=np.float64)
+    piv = np.zeros(p * p * b, dtype=np.int32)
+    info = lib().o_lu_nopiv(n, b, ib, _d(tiles), _d(Ls), _i(piv))
+    return Ls, piv, info
+
+
+def ref_genp(A):
+    """Unblocked GENP (textbook): returns (LU packed, info)."""
+    A = np.asfortranarray(A, dtype=np.float64).copy(order="F")
+    info = lib().o_ref_genp(A.shape[0], _d(A))
+    return A, info
+
+
+def _rhs(X):
+    X = np.asfortranarray(X, dtype=np.float64).copy(order="F")
+    return X.reshape(-1, 1, order="F") if X.ndim == 1 else X
+
+
+def trsm_upper(F, X, n, b):
+    """X <- U^{-1} X with U the upper triangle of BDL F (back substitution)."""
+    X = _rhs(X)
+    lib().o_trsm_upper_bdl(n, b, _d(np.ascontiguousarray(F)), _d(X), X.shape[1], X.shape[0])
+    return X
+
+
+def lu_solve(F, Ls, piv, X, n, b, ib):
+    """X <- A^{-1} X = U^{-1} N^{-1} X with the factors of Algorithm 3."""
+    X = _rhs(X)
+    lib().o_lu_solve(n, b, ib, _d(np.ascontiguousarray(F)), _d(np.ascontiguousarray(Ls)),
+                     _i(np.ascontiguousarray(piv)), _d(X), X.shape[1], X.shape[0])
+    return X
+
+
+def qr_solve(F, T, X, n, b, ib):
+    """X <- A^{-1} X = R^{-1} Q^T X with the factors of Algorithm 2."""
+    return trsm_upper(F, qr_apply(F, T, X, n, b, ib, trans=True), n, b)
 
 
 def lu_decisions(tiles: np.ndarray, n: int, b: int, ib: int):

@@ -376,6 +376,11 @@ static void o_swap_rows(double* X, int64_t ld, int64_t r1, int64_t r2, int64_t c
   }
 }
 
+/* Pivoting switch for GENP (Gaussian elimination with no pivoting):
+ * when set, o_getrf keeps row j and o_tstrf keeps the top row for every column; the
+ * arithmetic is otherwise that of Algorithm 3.  Only o_lu_nopiv sets it. */
+static int o_nopiv = 0;
+
 /* Pivot-decision recorder — test instrumentation for the C5 seed-margin reading
  * (DESIGN.md §3): when armed, every pivot decision of o_getrf /
  * o_tstrf appends (|winner|, |runner-up|) in program order.  It only reads the
@@ -399,7 +404,7 @@ void o_getrf(int64_t b, int64_t ib, double* A, int32_t* ipiv, int* info) {
     for (int64_t j = c0; j < c1; ++j) {
       int64_t r = j;
       double best = fabs(OE(A, b, j, j));
-      for (int64_t rr = j + 1; rr < b; ++rr)
+      for (int64_t rr = j + 1; rr < b && !o_nopiv; ++rr)
         if (fabs(OE(A, b, rr, j)) > best) { best = fabs(OE(A, b, rr, j)); r = rr; }
       if (o_dec) {
         double second = -1.0;
@@ -469,7 +474,7 @@ void o_tstrf(int64_t b, int64_t ib, double* U, double* A, double* Ls, int32_t* i
     for (int64_t j = c0; j < c1; ++j) {
       int64_t r = -1;
       double best = fabs(OE(U, b, j, j));
-      for (int64_t rr = 0; rr < b; ++rr)
+      for (int64_t rr = 0; rr < b && !o_nopiv; ++rr)
         if (fabs(OE(A, b, rr, j)) > best) { best = fabs(OE(A, b, rr, j)); r = rr; }
       if (o_dec) {
         double second = (r >= 0) ? fabs(OE(U, b, j, j)) : -1.0;
@@ -572,6 +577,90 @@ int o_lu(int64_t n, int64_t b, int64_t ib, double* A, double* Ls, int32_t* ipiv)
   return (int)best;
 }
 
+/* GENP in tiled form: Algorithm 3 with every pivot kept (o_nopiv).
+ * Pivots come out as the identity encodings (j + 1). */
+int o_lu_nopiv(int64_t n, int64_t b, int64_t ib, double* A, double* Ls, int32_t* ipiv) {
+  o_nopiv = 1;
+  int info = o_lu(n, b, ib, A, Ls, ipiv);
+  o_nopiv = 0;
+  return info;
+}
+
+/* X (n x ncol, ld ldx) <- U^{-1} X with U the upper triangle of the BDL matrix F (tiles
+ * j >= i; R of Algorithm 2 or U of Algorithm 3): textbook back substitution, row by row
+ * from the bottom, x[r] = (x[r] - sum_{m>r} U[r,m] x[m]) / U[r,r]. */
+void o_trsm_upper_bdl(int64_t n, int64_t b, const double* F, double* X, int64_t ncol, int64_t ldx) {
+  int64_t p = n / b;
+  for (int64_t c = 0; c < ncol; ++c)
+    for (int64_t r = n - 1; r >= 0; --r) {
+      double acc = OE(X, ldx, r, c);
+      for (int64_t m = r + 1; m < n; ++m)
+        acc -= OE(OT(F, p, b, r / b, m / b), b, r % b, m % b) * OE(X, ldx, m, c);
+      OE(X, ldx, r, c) = acc / OE(OT(F, p, b, r / b, r / b), b, r % b, r % b);
+    }
+}
+
+/* Solve with the factors of Algorithm 3 (Eq. eq:GETWPcompact, N U = A):
+ * X <- A^{-1} X = U^{-1} N^{-1} X.  N^{-1} X applies the elimination steps to X in program
+ * order — for each k the DGESSM step on tile row k (all swaps, then the blocked unit-lower
+ * solve), then for i > k the DSSSSM step on tile rows (k, i) (per inner block: swaps,
+ * (I + Ls_s)^{-1} on the top rows, bottom -= L_ik[:, s] top) — exactly the operations the
+ * factorization applies to the columns right of panel k (C3); then back substitution. */
+void o_lu_solve(int64_t n, int64_t b, int64_t ib, const double* F, const double* Ls, const int32_t* ipiv,
+                double* X, int64_t ncol, int64_t ldx) {
+  int64_t p = n / b;
+  for (int64_t k = 0; k < p; ++k) {
+    double* xk = X + k * b;
+    const double* Lkk = OT(F, p, b, k, k);
+    const int32_t* pk = OPIV(ipiv, p, b, k, k);
+    for (int64_t j = 0; j < b; ++j) o_swap_rows(xk, ldx, j, pk[j] - 1, 0, ncol);
+    for (int64_t s = 0; s * ib < b; ++s) {
+      int64_t c0 = s * ib, c1 = c0 + ib;
+      for (int64_t c = 0; c < ncol; ++c)
+        for (int64_t r = c0; r < c1; ++r) {
+          double acc = OE(xk, ldx, r, c);
+          for (int64_t m = c0; m < r; ++m) acc -= OE(Lkk, b, r, m) * OE(xk, ldx, m, c);
+          OE(xk, ldx, r, c) = acc;
+        }
+      for (int64_t c = 0; c < ncol; ++c)
+        for (int64_t r = c1; r < b; ++r) {
+          double acc = OE(xk, ldx, r, c);
+          for (int64_t m = c0; m < c1; ++m) acc -= OE(Lkk, b, r, m) * OE(xk, ldx, m, c);
+          OE(xk, ldx, r, c) = acc;
+        }
+    }
+    for (int64_t i = k + 1; i < p; ++i) {
+      double* xi = X + i * b;
+      const double* L = OT(F, p, b, i, k);
+      const double* Lst = OSTRIP(Ls, p, b, ib, i, k);
+      const int32_t* pv = OPIV(ipiv, p, b, i, k);
+      for (int64_t s = 0; s * ib < b; ++s) {
+        int64_t c0 = s * ib, c1 = c0 + ib;
+        for (int64_t j = c0; j < c1; ++j)
+          if (pv[j] > b) {
+            int64_t r = pv[j] - b - 1;
+            for (int64_t c = 0; c < ncol; ++c) {
+              double tmp = OE(xk, ldx, j, c); OE(xk, ldx, j, c) = OE(xi, ldx, r, c); OE(xi, ldx, r, c) = tmp;
+            }
+          }
+        for (int64_t c = 0; c < ncol; ++c)
+          for (int64_t r = c0; r < c1; ++r) {
+            double acc = OE(xk, ldx, r, c);
+            for (int64_t m = c0; m < r; ++m) acc -= OE(Lst, ib, r - c0, m) * OE(xk, ldx, m, c);
+            OE(xk, ldx, r, c) = acc;
+          }
+        for (int64_t c = 0; c < ncol; ++c)
+          for (int64_t r = 0; r < b; ++r) {
+            double acc = OE(xi, ldx, r, c);
+            for (int64_t m = c0; m < c1; ++m) acc -= OE(L, b, r, m) * OE(xk, ldx, m, c);
+            OE(xi, ldx, r, c) = acc;
+          }
+      }
+    }
+  }
+  o_trsm_upper_bdl(n, b, F, X, ncol, ldx);
+}
+
 /* C4 / Eq. (eq:formula N), (eq:GETWPcompact):
  * X (n x ncol, ld n) <- N X, N = (prod of the elementary L and P of GETWP)^{-1},
  * applied implicitly by undoing every elimination step in reverse program order. */
@@ -671,6 +760,23 @@ int o_ref_gepp(int64_t n, double* A, int32_t* ipiv) {
     ipiv[j] = (int32_t)(r + 1);
     if (OE(A, n, r, j) != 0.0) {
       o_swap_rows(A, n, j, r, 0, n);
+      for (int64_t rr = j + 1; rr < n; ++rr) OE(A, n, rr, j) /= OE(A, n, j, j);
+    } else if (!info) {
+      info = (int)(j + 1);
+    }
+    for (int64_t c = j + 1; c < n; ++c)
+      for (int64_t rr = j + 1; rr < n; ++rr) OE(A, n, rr, c) -= OE(A, n, rr, j) * OE(A, n, j, c);
+  }
+  return info;
+}
+
+/* GENP — Gaussian elimination with no pivoting, unblocked textbook
+ * right-looking form: L strictly lower (multipliers), U upper.  Returns info (first zero
+ * pivot, 1-based). */
+int o_ref_genp(int64_t n, double* A) {
+  int info = 0;
+  for (int64_t j = 0; j < n; ++j) {
+    if (OE(A, n, j, j) != 0.0) {
       for (int64_t rr = j + 1; rr < n; ++rr) OE(A, n, rr, j) /= OE(A, n, j, j);
     } else if (!info) {
       info = (int)(j + 1);

@@ -207,6 +207,7 @@ struct Addr {
     if (D.pptr) return D.pptr[i + (size_t)k * P.p];
     return P.ipiv + ((size_t)i + (size_t)k * P.p) * P.b;
   }
+  __device__ double* X(int i, int c) const { return P.X + ((size_t)i + (size_t)c * P.p) * (size_t)P.b * P.b; }
   __device__ double* VX(int k) const {
     TF_ASSERT(!D.vptr || D.vptr[k], "rank %d: null VX(%d)", D.rank, k);
     if (D.vptr) return D.vptr[k];
@@ -315,6 +316,16 @@ __device__ inline void run_item(const Prob& P, const Sched& S, const Dist& D, co
       if (f >= 0 && threadIdx.x == 0) atomicMin(cx.info, k * P.b + f + 1);
     } break;
     case 11: ssssm_item(cx, a.T(i, k), a.STRIP(i, k), a.PIV(i, k), a.T(k, j), a.T(i, j), sub, sm); break;
+    // solve / apply tasks (tf_solve.cuh); d.j = the right-hand-side tile column c
+    case K_UNITL: unitl_item(cx, a.T(k, k), a.VX(k)); break;
+    case K_XGESSM: gessm_item(cx, a.VX(k), a.PIV(k, k), a.X(k, j), sub, sm); break;
+    case K_XSSSSM: ssssm_item(cx, a.T(i, k), a.STRIP(i, k), a.PIV(i, k), a.X(k, j), a.X(i, j), sub, sm); break;
+    case K_XLARFB: larfb_item(cx, a.VX(k), a.STRIP(k, k), a.X(k, j), sub, sm); break;
+    case K_XSSRFB: ssrfb_item(cx, a.T(i, k), a.STRIP(i, k), a.X(k, j), a.X(i, j), sub, sm); break;
+    case K_XTRSMU: v_trsmu(cx, a.T(k, k), a.X(k, j), sub); break;
+    case K_XGEMM: v_xgemm(cx, a.T(i, k), a.X(k, j), a.X(i, j), sub); break;
+    case K_XUNSSSSM: v_unssssm(cx, a.T(i, k), a.STRIP(i, k), a.PIV(i, k), a.X(k, j), a.X(i, j), sub); break;
+    case K_XUNGESSM: v_ungessm(cx, a.T(k, k), a.PIV(k, k), a.X(k, j), sub); break;
     case K_SEND: send_item(a, d, sub); break;
     case K_RECV: break;  // the data is already in the cache; completing releases the consumers
     default: break;
@@ -350,6 +361,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1) tf_persistent(const __grid_cons
   cx.scratch = P.scratch + (size_t)(blockIdx.x - D.cta0) * P.scr_stride;
   cx.info = P.info;
   cx.abort_flag = S.abort_flag;
+  cx.nopiv = P.nopiv;
   pipe_init(sm);
   if (D.nranks > 0) {
     // start barrier: no peer may push into this rank's queues before it has been reset
@@ -468,6 +480,19 @@ __global__ void pack_kernel(int64_t m, int64_t n, int64_t b, double* D, double* 
   }
 }
 
+// Right-hand sides: dense column-major X (n x nrhs, ld ldx) <-> BDL tiles of an n x q*b
+// matrix (tile (i,c) at (i + c*p)*b*b), padding columns >= nrhs with zeros.
+__global__ void xpack_kernel(int64_t n, int64_t nrhs, int64_t ldx, int64_t b, int64_t q, double* X, double* T,
+                             int dir) {
+  const int64_t p = n / b, bb = b * b, tot = n * q * b;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = e / bb, w = e % bb;
+    const int64_t r = (t % p) * b + w % b, c = (t / p) * b + w / b;
+    if (dir == 0) T[e] = c < nrhs ? X[r + c * ldx] : 0.0;
+    else if (c < nrhs) X[r + c * ldx] = T[e];
+  }
+}
+
 // IPC path check (tile_dist_probe): one system-scope release store of `value` into the
 // peer's probe slot for this rank and one system-scope atomic on its probe counter.
 __global__ void probe_kernel(int* peer_sync, int rank, int value) {
@@ -509,6 +534,11 @@ int launch_persistent(const Runs& R, int ctas, size_t smem, void* stream, bool c
 }
 int launch_probe(char* peer_sym, int rank, int value, void* stream) {
   probe_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(reinterpret_cast<int*>(peer_sym), rank, value);
+  return ok_or(cudaGetLastError());
+}
+int launch_xpack(int64_t n, int64_t nrhs, int64_t ldx, int64_t b, int64_t q, double* X, double* T, int dir,
+                 void* stream) {
+  xpack_kernel<<<1184, 256, 0, (cudaStream_t)stream>>>(n, nrhs, ldx, b, q, X, T, dir);
   return ok_or(cudaGetLastError());
 }
 int launch_pack(int64_t m, int64_t n, int64_t b, double* D, double* T, int dir, void* stream) {

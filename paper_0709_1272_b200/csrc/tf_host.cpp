@@ -72,6 +72,9 @@ inline uint64_t key4(int kind, int k, int i, int j) {
 
 int level_of(int kind, int k, int j, int policy) {
   switch (kind) {
+    case K_UNITL: case K_XTRSMU: case K_XGESSM: case K_XLARFB: case K_XUNGESSM: return 1;
+    case K_XSSSSM: case K_XSSRFB: case K_XUNSSSSM: return 2;
+    case K_XGEMM: return 3;
     case 0: case 4: case 8: case K_SEND: case K_RECV: return 0;  // panel (and panel traffic)
     case 1: case 6: case 10: return 1;     // couple-factor (TRSM for Cholesky)
     case 5: case 9: return 2;              // row-update
@@ -146,6 +149,74 @@ void global_tasks(int alg, int p, int b, int ib, int policy, std::vector<TaskD>&
   }
 }
 
+// Solve / apply DAGs (NEXT-3) over the right-hand-side tiles X(i,c), c < q.  The factor
+// tiles are read-only inputs, so dependencies come from the X tiles and the explicit
+// unit-lower copies VX(k) only; they are derived generically (read-after-write,
+// write-after-read, write-after-write on each tile, tasks in program order), which is
+// correct by construction for any task order below.
+//   getrs: N^{-1} X (XGESSM(k), XSSSSM(i>k,k): Algorithm 3's updates on extra columns),
+//          then U^{-1} X (XTRSMU(k), XGEMM(i<k,k), k descending)
+//   ormqr: Q^T X (XLARFB(k), XSSRFB(i>k,k): Algorithm 2's updates on extra columns)
+//   qrs:   ormqr, then R^{-1} X as getrs' second half
+//   lu_apply_N: N X = every elimination step undone in reverse program order (C4)
+void solve_tasks(int alg, int p, int b, int ib, int q, int policy, std::vector<TaskD>& tasks,
+                 std::vector<std::vector<int>>& preds) {
+  struct Acc { int tile; bool w; };
+  std::vector<std::vector<Acc>> acc;
+  tasks.clear();
+  const int VXB = p * q;  // tile ids: X(i,c) = i + c*p, VX(k) = VXB + k
+  auto X = [&](int i, int c) { return i + c * p; };
+  auto add = [&](int kind, int k, int i, int j, std::vector<Acc> a) {
+    tasks.push_back(TaskD{kind, k, i, j, items_of(kind, b, ib), 0, level_of(kind, k, j, policy), 0});
+    acc.push_back(std::move(a));
+  };
+  const bool lu = alg == ALG_GETRS || alg == ALG_LUN;
+  if (alg == ALG_GETRS || alg == ALG_ORMQR || alg == ALG_QRS) {
+    for (int k = 0; k < p; ++k) add(K_UNITL, k, k, k, {{VXB + k, true}});
+    for (int k = 0; k < p; ++k) {
+      for (int c = 0; c < q; ++c)
+        add(lu ? K_XGESSM : K_XLARFB, k, k, c, {{VXB + k, false}, {X(k, c), true}});
+      for (int i = k + 1; i < p; ++i)
+        for (int c = 0; c < q; ++c) add(lu ? K_XSSSSM : K_XSSRFB, k, i, c, {{X(k, c), true}, {X(i, c), true}});
+    }
+  }
+  if (alg == ALG_GETRS || alg == ALG_QRS) {
+    for (int k = p - 1; k >= 0; --k)
+      for (int c = 0; c < q; ++c) {
+        add(K_XTRSMU, k, k, c, {{X(k, c), true}});
+        for (int i = 0; i < k; ++i) add(K_XGEMM, k, i, c, {{X(k, c), false}, {X(i, c), true}});
+      }
+  }
+  if (alg == ALG_LUN) {
+    for (int k = p - 1; k >= 0; --k)
+      for (int c = 0; c < q; ++c) {
+        for (int i = p - 1; i > k; --i) add(K_XUNSSSSM, k, i, c, {{X(k, c), true}, {X(i, c), true}});
+        add(K_XUNGESSM, k, k, c, {{X(k, c), true}});
+      }
+  }
+  const int nt = (int)tasks.size();
+  preds.assign(nt, {});
+  std::unordered_map<int, int> last_w;
+  std::unordered_map<int, std::vector<int>> readers;
+  for (int t = 0; t < nt; ++t) {
+    auto& pr = preds[t];
+    for (const Acc& a : acc[t]) {
+      auto lw = last_w.find(a.tile);
+      if (lw != last_w.end()) pr.push_back(lw->second);
+      if (!a.w) {
+        readers[a.tile].push_back(t);
+      } else {
+        for (int r : readers[a.tile])
+          if (r != t) pr.push_back(r);
+        readers[a.tile].clear();
+        last_w[a.tile] = t;
+      }
+    }
+    std::sort(pr.begin(), pr.end());
+    pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
+  }
+}
+
 // CSR successors, in-degrees, work items, per-level queue bases and roots.
 void finalize_dag(HostDag& G, const std::vector<std::vector<int>>& preds) {
   const int nt = (int)G.tasks.size();
@@ -178,10 +249,11 @@ void finalize_dag(HostDag& G, const std::vector<std::vector<int>>& preds) {
     if (G.indeg0[t] == 0 && G.tasks[t].kind != K_RECV) G.roots.push_back(t);
 }
 
-void build_dag(HostDag& G, int alg, int p, int b, int ib, int policy) {
+void build_dag(HostDag& G, int alg, int p, int b, int ib, int policy, int q = 0) {
   G.alg = alg; G.p = p; G.b = b; G.policy = policy;
   std::vector<std::vector<int>> preds;
-  global_tasks(alg, p, b, ib, policy, G.tasks, preds);
+  if (alg >= ALG_GETRS) solve_tasks(alg, p, b, ib, q, policy, G.tasks, preds);
+  else global_tasks(alg, p, b, ib, policy, G.tasks, preds);
   finalize_dag(G, preds);
 }
 
@@ -310,7 +382,7 @@ struct DevDag {
   SendEnt* sends = nullptr;
 };
 
-std::map<std::tuple<int, int, int, int, int, int>, DevDag> g_dags;  // (dev, alg, p, b, ib, policy)
+std::map<std::tuple<int, int, int, int, int, int, int>, DevDag> g_dags;  // (dev, alg, p, b, ib, policy, q)
 
 template <class T>
 int upload(T** dst, const std::vector<T>& v) {
@@ -341,13 +413,13 @@ void free_dag(DevDag& D) {
   D = DevDag();
 }
 
-int get_dag(int dev, int alg, int p, int b, int ib, DevDag** out) {
-  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy);
+int get_dag(int dev, int alg, int p, int b, int ib, DevDag** out, int q = 0) {
+  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy, q);
   auto it = g_dags.find(key);
   if (it != g_dags.end()) { *out = &it->second; return 0; }
   DevDag D;
   D.h = std::make_shared<HostDag>();
-  build_dag(*D.h, alg, p, b, ib, g_policy);
+  build_dag(*D.h, alg, p, b, ib, g_policy, q);
   int rc;
   if ((rc = upload_dag(D))) return rc;
   auto res = g_dags.emplace(key, D);
@@ -379,7 +451,7 @@ void release(Buf& b) {
 }
 
 struct Workspace {
-  Buf state, q, vx, scratch, info, trace;
+  Buf state, q, vx, scratch, info, trace, xt;
   Buf hostA, hostAux, hostPiv;  // device buffers for tile_factor_host
   int64_t last_items = 0;
   cudaStream_t stream = nullptr;
@@ -447,7 +519,7 @@ long long watchdog_ns() {
 }
 
 int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, double* aux, int32_t* ipiv,
-                      int32_t* d_info, cudaStream_t stream) {
+                      int32_t* d_info, cudaStream_t stream, double* X = nullptr, int q = 0, int nopiv = 0) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   int dev;
   TF_CUDA(cudaGetDevice(&dev));
@@ -455,7 +527,7 @@ int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, dou
   if ((rc = device_setup(dev))) return rc;
   const int p = (int)(n / b);
   DevDag* D;
-  if ((rc = get_dag(dev, alg, p, (int)b, (int)ib, &D))) return rc;
+  if ((rc = get_dag(dev, alg, p, (int)b, (int)ib, &D, q))) return rc;
   const HostDag& H = *D->h;
   Workspace& W = g_ws[std::make_pair(dev, stream)];
   W.stream = stream;
@@ -464,7 +536,7 @@ int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, dou
   const size_t state_ints = (size_t)2 * (nt + 4) + 2 * NLEV + 8;
   if ((rc = ensure(W.state, state_ints * sizeof(int)))) return rc;
   if ((rc = ensure(W.q, (size_t)H.nitems * sizeof(int)))) return rc;
-  if (alg != 0 && (rc = ensure(W.vx, (size_t)p * b * b * sizeof(double)))) return rc;
+  if (alg != 0 && alg != ALG_LUN && (rc = ensure(W.vx, (size_t)p * b * b * sizeof(double)))) return rc;
   const size_t scr = scr_stride_for((int)b, (int)ib);
   if ((rc = ensure(W.scratch, scr * ctas * sizeof(double)))) return rc;
   if ((rc = ensure(W.info, 64))) return rc;
@@ -489,6 +561,9 @@ int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, dou
   P.ib = (int)ib;
   P.p = p;
   P.info = d_info ? d_info : (int*)W.info.p;
+  P.X = X;
+  P.q = q;
+  P.nopiv = nopiv;
   R.r[0].D.timeout_ns = watchdog_ns();
   TF_LAUNCH(launch_sched_reset(S, D->indeg0, H.nitems, P.info, stream));
   TF_LAUNCH(launch_sched_seed(S, D->roots, (int)H.roots.size(), stream));
@@ -725,6 +800,65 @@ int tile_lu(int64_t n, int64_t b, int64_t ib, double* dA, double* dLs, int32_t* 
   return run_factorization(2, n, b, ib, dA, dLs, dIpiv, d_info, (cudaStream_t)stream);
 }
 
+// Solve / apply entry points (NEXT-3): X (n x nrhs, ld ldx, device) is packed into library
+// BDL scratch, the solve DAG runs on the persistent scheduler, X is unpacked; all async on
+// `stream` (the scratch is per (device, stream), so calls on one stream serialize).
+static int run_solve(int alg, int64_t n, int64_t b, int64_t ib, const double* dF, const double* dAux,
+                     const int32_t* dIpiv, int64_t nrhs, double* dX, int64_t ldx, tf_stream_t stream) {
+  int rc = check_args(n, b, ib, dF);
+  if (rc) return rc;
+  if (!dAux) { set_err("null T / L-strip pointer"); return -5; }
+  const bool lu = alg == ALG_GETRS || alg == ALG_LUN;
+  if (lu && !dIpiv) { set_err("null ipiv pointer"); return -6; }
+  if (nrhs < 0) { set_err("nrhs < 0"); return -7; }
+  if (nrhs == 0) return 0;
+  if (!dX) { set_err("null X pointer"); return -8; }
+  if (ldx < n) { set_err("ldx < n"); return -9; }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t q = (nrhs + b - 1) / b;
+  if (q > (1 << 16)) { set_err("too many right-hand sides"); return -7; }
+  int dev;
+  TF_CUDA(cudaGetDevice(&dev));
+  Workspace* W;
+  {
+    std::lock_guard<std::recursive_mutex> lk(g_mu);
+    W = &g_ws[std::make_pair(dev, s)];
+    if ((rc = ensure(W->xt, (size_t)n * q * b * sizeof(double)))) return rc;
+  }
+  double* Xt = (double*)W->xt.p;
+  TF_LAUNCH(launch_xpack(n, nrhs, ldx, b, q, dX, Xt, 0, s));
+  if ((rc = run_factorization(alg, n, b, ib, const_cast<double*>(dF), const_cast<double*>(dAux),
+                              const_cast<int32_t*>(dIpiv), nullptr, s, Xt, (int)q)))
+    return rc;
+  TF_LAUNCH(launch_xpack(n, nrhs, ldx, b, q, dX, Xt, 1, s));
+  return 0;
+}
+
+int tile_getrs(int64_t n, int64_t b, int64_t ib, const double* dF, const double* dLs, const int32_t* dIpiv,
+               int64_t nrhs, double* dX, int64_t ldx, tf_stream_t stream) {
+  return run_solve(ALG_GETRS, n, b, ib, dF, dLs, dIpiv, nrhs, dX, ldx, stream);
+}
+int tile_ormqr(int64_t n, int64_t b, int64_t ib, const double* dF, const double* dT, int64_t nrhs, double* dX,
+               int64_t ldx, tf_stream_t stream) {
+  return run_solve(ALG_ORMQR, n, b, ib, dF, dT, nullptr, nrhs, dX, ldx, stream);
+}
+int tile_qrs(int64_t n, int64_t b, int64_t ib, const double* dF, const double* dT, int64_t nrhs, double* dX,
+             int64_t ldx, tf_stream_t stream) {
+  return run_solve(ALG_QRS, n, b, ib, dF, dT, nullptr, nrhs, dX, ldx, stream);
+}
+int tile_lu_apply_N(int64_t n, int64_t b, int64_t ib, const double* dF, const double* dLs, const int32_t* dIpiv,
+                    int64_t nrhs, double* dX, int64_t ldx, tf_stream_t stream) {
+  return run_solve(ALG_LUN, n, b, ib, dF, dLs, dIpiv, nrhs, dX, ldx, stream);
+}
+int tile_lu_nopiv(int64_t n, int64_t b, int64_t ib, double* dA, double* dLs, int32_t* dIpiv, int32_t* d_info,
+                  tf_stream_t stream) {
+  int rc = check_args(n, b, ib, dA);
+  if (rc) return rc;
+  if (!dLs) { set_err("null L-strip pointer"); return -5; }
+  if (!dIpiv) { set_err("null ipiv pointer"); return -6; }
+  return run_factorization(2, n, b, ib, dA, dLs, dIpiv, d_info, (cudaStream_t)stream, nullptr, 0, 1);
+}
+
 size_t tile_qr_t_elems(int64_t n, int64_t b, int64_t ib) {
   if (n <= 0 || b <= 0 || n % b) return 0;
   const size_t p = n / b;
@@ -811,9 +945,9 @@ int64_t tile_trace_fetch(int64_t* rec, int64_t cap) {
 int64_t tile_dag_export(int alg, int64_t p, int policy, int32_t* kind, int32_t* k, int32_t* i, int32_t* j,
                         int32_t* level, int64_t cap, int64_t* succ_off, int32_t* succ, int64_t succ_cap,
                         int64_t* nedges) {
-  if (alg < 0 || alg > 2 || p <= 0) return -1;
+  if (alg < 0 || alg > ALG_LUN || p <= 0) return -1;
   HostDag G;
-  build_dag(G, alg, (int)p, 128, 32, policy);
+  build_dag(G, alg, (int)p, 128, 32, policy, alg >= ALG_GETRS ? 1 : 0);
   const int64_t nt = (int64_t)G.tasks.size();
   for (int64_t t = 0; t < nt && t < cap; ++t) {
     if (kind) kind[t] = G.tasks[t].kind;
@@ -1071,7 +1205,7 @@ void tile_finalize(void) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   for (auto& kv : g_ws) {
     Workspace& W = kv.second;
-    for (Buf* b : {&W.state, &W.q, &W.vx, &W.scratch, &W.info, &W.trace, &W.hostA, &W.hostAux, &W.hostPiv})
+    for (Buf* b : {&W.state, &W.q, &W.vx, &W.scratch, &W.info, &W.trace, &W.xt, &W.hostA, &W.hostAux, &W.hostPiv})
       release(*b);
   }
   g_ws.clear();

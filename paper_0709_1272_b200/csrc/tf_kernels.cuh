@@ -31,6 +31,7 @@ struct Ctx {
   double* scratch;  // this CTA's global scratch (>= 2*ib*b + 64 doubles)
   int* info;        // INT_MAX = no failure; atomicMin of the 1-based global column
   int* abort_flag;  // set on Cholesky failure: the scheduler stops handing out work
+  int nopiv;        // LU without pivoting (GENP): every pivot is kept
 };
 
 // Kernel variants (register-slab kernel at one tile size, or the reference-blocked path):
@@ -842,7 +843,7 @@ __device__ inline int getrf_ref(const Ctx& cx, double* A, int* ipiv, double* LX,
     for (int j = c0; j < c1; ++j) {
       double v = -1.0;
       int idx = INT_MAX;
-      for (int r = j + tid; r < b; r += TF_THREADS) amax_merge(v, idx, fabs(A[r + (size_t)j * b]), r);
+      for (int r = j + tid; r < (cx.nopiv ? j + 1 : b); r += TF_THREADS) amax_merge(v, idx, fabs(A[r + (size_t)j * b]), r);
       const int pr = block_amax(v, idx, redv, redi);
       const double pv = A[pr + (size_t)j * b];
       __syncthreads();
@@ -939,14 +940,14 @@ __device__ inline void gessm_ref(const Ctx& cx, const double* LX, const int* ipi
 // ldp), top Ub (ib x ib, ld ib, upper = U[c0:c1, c0:c1]), L-strip block Lsb (ld ib,
 // zeroed), pivots piv[0..ib) (global, 1-based in [1, 2b]).  Returns first zero column.
 __device__ inline int tstrf_panel(double* P, int ldp, int b, double* Ub, double* Lsb, int ib, int c0, int* piv,
-                                  double* redv, int* redi) {
+                                  double* redv, int* redi, int nopiv) {
   const int tid = threadIdx.x;
   int first_zero = -1;
   for (int jj = 0; jj < ib; ++jj) {
     double v = -1.0;
     int idx = INT_MAX;
     if (tid == 0) { v = fabs(Ub[jj + jj * ib]); idx = -1; }
-    for (int r = tid; r < b; r += TF_THREADS) amax_merge(v, idx, fabs(P[r + (size_t)jj * ldp]), r);
+    for (int r = tid; r < (nopiv ? 0 : b); r += TF_THREADS) amax_merge(v, idx, fabs(P[r + (size_t)jj * ldp]), r);
     const int pr = block_amax(v, idx, redv, redi);
     if (pr >= 0) {
       for (int c = jj + tid; c < ib; c += TF_THREADS) {
@@ -1002,7 +1003,7 @@ __device__ inline int tstrf_ref(const Ctx& cx, double* U, double* A, double* Ls,
       P = A + (size_t)c0 * b;
     }
     __syncthreads();
-    const int fz = tstrf_panel(P, b, b, Ub, Lsb, ib, c0, ipiv + c0, redv, redi);
+    const int fz = tstrf_panel(P, b, b, Ub, Lsb, ib, c0, ipiv + c0, redv, redi, cx.nopiv);
     if (fz >= 0 && first_zero < 0) first_zero = c0 + fz;
     if (in_smem)
       for (int e = tid; e < b * ib; e += TF_THREADS) A[(size_t)c0 * b + e] = P[e];
@@ -1058,6 +1059,7 @@ __device__ inline void ssssm_ref(const Ctx& cx, const double* L, const double* L
 
 }  // namespace tf
 #include "tf_lu_slab.cuh"
+#include "tf_solve.cuh"
 namespace tf {
 
 TF_DEF_VARIANT(v_gessm_reg, gessm_reg, (Ctx cx, const double* LX, const int* ipiv, double* C, int item),
@@ -1093,6 +1095,15 @@ __device__ inline int getrf_item(const Ctx& cx, double* A, int* ipiv, double* LX
   if (ssrfb_reg_ok(cx.b, cx.ib)) return TF_SLAB_RET(v_getrf_slab, cx, A, ipiv, LX);
   return v_getrf_ref(cx, A, ipiv, LX);
 }
+TF_DEF_REF(v_trsmu, trsmu_item, (Ctx cx, const double* U, double* X, int item), (cx, U, X, item, dsm))
+TF_DEF_REF(v_xgemm, xgemm_item, (Ctx cx, const double* A, const double* B, double* C, int item),
+           (cx, A, B, C, item, dsm))
+TF_DEF_REF(v_unssssm, unssssm_item,
+           (Ctx cx, const double* L, const double* Ls, const int* ipiv, double* X1, double* X2, int item),
+           (cx, L, Ls, ipiv, X1, X2, item, dsm))
+TF_DEF_REF(v_ungessm, ungessm_item, (Ctx cx, const double* F, const int* ipiv, double* X, int item),
+           (cx, F, ipiv, X, item, dsm))
+
 __device__ inline int tstrf_item(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, double* sm) {
   if (ssrfb_reg_ok(cx.b, cx.ib)) return TF_SLAB_RET(v_tstrf_slab, cx, U, A, Ls, ipiv);
   return v_tstrf_ref(cx, U, A, Ls, ipiv);

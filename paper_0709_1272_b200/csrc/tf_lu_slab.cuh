@@ -398,7 +398,7 @@ __device__ __forceinline__ void warp_first_max(double v, int idx, double& bv, in
 }
 
 template <int MI, bool TS>
-__device__ inline int lu_panel(double* P, int ldp, int cs, int b, double* UL, int* piv, double* sm2) {
+__device__ inline int lu_panel(double* P, int ldp, int cs, int b, double* UL, int* piv, double* sm2, int nopiv) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwa = (b + 31) >> 5;                         // warps that own rows
   const bool own = tid < b;
@@ -419,7 +419,8 @@ __device__ inline int lu_panel(double* P, int ldp, int cs, int b, double* UL, in
     // after it, while slower warps may still be comparing
     const double top = TS ? fabs(UL[jj * 33 + jj]) : 0.0;
     if (warp < nwa) {
-      const bool cand = own && (TS || tid >= cg);
+      // GENP (nopiv): GETRF's only candidate is row cg; TSTRF keeps the top row
+      const bool cand = own && (TS ? !nopiv : (nopiv ? tid == cg : tid >= cg));
       double wv;
       int wi;
       warp_first_max(cand ? fabs(x[jj]) : 0.0, cand ? tid : INT_MAX, wv, wi);
@@ -541,7 +542,7 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
     }
     __syncthreads();
     TF_LU_T(9);
-    const int fz = lu_panel<MI, true>(P, ldp, cs, b, UL, ipiv + cs, sm2);
+    const int fz = lu_panel<MI, true>(P, ldp, cs, b, UL, ipiv + cs, sm2, cx.nopiv);
     if (fz >= 0 && first_zero < 0) first_zero = cs + fz;
     TF_LU_T(10);
     for (int e = tid; e < b * 32; e += TF_THREADS) {
@@ -611,7 +612,7 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
         for (int e = 0; e < 2; ++e) P[(r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * ldp] = acc[i][j][e];
     __syncthreads();
     TF_LU_T(2);
-    const int fz = lu_panel<MI, false>(P, ldp, cs, b, nullptr, ipiv + cs, sm2);
+    const int fz = lu_panel<MI, false>(P, ldp, cs, b, nullptr, ipiv + cs, sm2, cx.nopiv);
     if (fz >= 0 && first_zero < 0) first_zero = cs + fz;
     TF_LU_T(3);
     for (int e = tid; e < b * 32; e += TF_THREADS) {

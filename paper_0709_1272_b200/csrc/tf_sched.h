@@ -29,7 +29,15 @@ constexpr int SEND_CHUNKS = 8;       // work items per (SEND task, peer)
 
 // task kinds: 0 POTRF 1 TRSM 2 SYRK 3 GEMM 4 GEQRT 5 LARFB 6 TSQRT 7 SSRFB
 //             8 GETRF 9 GESSM 10 TSTRF 11 SSSSM 12 SEND 13 RECV
+// solve / apply tasks on right-hand-side tiles X(i,c) (tf_solve.cuh; j = c):
+//             14 UNITL(k) 15 XGESSM(k,c) 16 XSSSSM(i,k,c) 17 XLARFB(k,c) 18 XSSRFB(i,k,c)
+//             19 XTRSMU(k,c) 20 XGEMM(i,k,c) 21 XUNSSSSM(i,k,c) 22 XUNGESSM(k,c)
 constexpr int K_SEND = 12, K_RECV = 13;
+constexpr int K_UNITL = 14, K_XGESSM = 15, K_XSSSSM = 16, K_XLARFB = 17, K_XSSRFB = 18, K_XTRSMU = 19,
+              K_XGEMM = 20, K_XUNSSSSM = 21, K_XUNGESSM = 22;
+// DAG algorithms: 0 chol, 1 qr, 2 lu (factorizations); 3 getrs (X <- A^{-1} X with LU
+// factors), 4 ormqr (X <- Q^T X), 5 qrs (X <- R^{-1} Q^T X), 6 lu_apply_N (X <- N X)
+constexpr int ALG_GETRS = 3, ALG_ORMQR = 4, ALG_QRS = 5, ALG_LUN = 6;
 
 TF_HD inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -57,7 +65,11 @@ TF_HD inline int items_of(int kind, int b, int ib) {
     case 1: return nr;                 // TRSM: row blocks
     case 2: return nr * (nr + 1) / 2;  // SYRK: lower sub-tiles
     case 3: return nr * nr / gemm_group(b);  // GEMM: groups of sub-tiles
-    case 5: case 7: case 9: case 11: return ssrfb_reg_ok(b, ib) ? b / NSR : ceil_div(b, NS);  // slabs
+    case 5: case 7: case 9: case 11:
+    case K_XGESSM: case K_XSSSSM: case K_XLARFB: case K_XSSRFB:
+      return ssrfb_reg_ok(b, ib) ? b / NSR : ceil_div(b, NS);  // slabs
+    case K_XTRSMU: case K_XUNSSSSM: case K_XUNGESSM: return ceil_div(b, 32);
+    case K_XGEMM: return ceil_div(b, 64);
     default: return 1;                 // panels, RECV
   }
 }
@@ -77,6 +89,9 @@ struct Prob {
   size_t scr_stride;
   int n, b, ib, p;
   int* info;     // INT_MAX = no failure (rank-local accumulator in multi-GPU mode)
+  double* X;     // solve / apply DAGs: right-hand sides in BDL, p x q tiles (tile (i,c) at (i + c*p)*b*b)
+  int q;
+  int nopiv;     // LU without pivoting (GENP)
 };
 
 struct Sched {
@@ -152,6 +167,8 @@ int launch_tk(int kind, int b, int ib, double* t0, double* t1, double* t2, doubl
 int launch_unit_lower(const double* A, double* X, int b, void* stream);
 int launch_pack(int64_t m, int64_t n, int64_t b, double* D, double* T, int dir, void* stream);
 int launch_probe(char* peer_sym, int rank, int value, void* stream);
+int launch_xpack(int64_t n, int64_t nrhs, int64_t ldx, int64_t b, int64_t q, double* X, double* T, int dir,
+                 void* stream);
 int device_kernel_setup(size_t smem);
 int tk_kernel_setup(size_t smem);
 size_t smem_bytes();

@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(TF_THREADS, 1)
   cx.scratch = scratch + (size_t)blockIdx.x * scr_stride;
   cx.info = info;
   cx.abort_flag = nullptr;
+  cx.nopiv = 0;
   pipe_init(sm);
   const int sub = blockIdx.x;
   int f = -1;

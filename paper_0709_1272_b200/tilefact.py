@@ -16,8 +16,10 @@ LIB_PATH = os.environ.get("TILEFACT_LIB") or os.path.join(_HERE, "libtilefact.so
 
 KINDS = {"potrf": 0, "trsm": 1, "syrk": 2, "gemm": 3, "geqrt": 4, "larfb": 5, "tsqrt": 6,
          "ssrfb": 7, "getrf": 8, "gessm": 9, "tstrf": 10, "ssssm": 11}
+SOLVE_KINDS = {"unitl": 14, "xgessm": 15, "xssssm": 16, "xlarfb": 17, "xssrfb": 18, "xtrsmu": 19, "xgemm": 20,
+               "xunssssm": 21, "xungessm": 22}
 KIND_NAMES = {v: k for k, v in KINDS.items()}
-ALGS = {"chol": 0, "qr": 1, "lu": 2}
+ALGS = {"chol": 0, "qr": 1, "lu": 2, "getrs": 3, "ormqr": 4, "qrs": 5, "lu_apply_N": 6}
 
 
 class TileFactError(RuntimeError):
@@ -34,6 +36,11 @@ def _load():
         "tile_chol": (i32, [i64, i64, i64, vp, vp, vp]),
         "tile_qr": (i32, [i64, i64, i64, vp, vp, vp]),
         "tile_lu": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),
+        "tile_lu_nopiv": (i32, [i64, i64, i64, vp, vp, vp, vp, vp]),
+        "tile_getrs": (i32, [i64, i64, i64, vp, vp, vp, i64, vp, i64, vp]),
+        "tile_ormqr": (i32, [i64, i64, i64, vp, vp, i64, vp, i64, vp]),
+        "tile_qrs": (i32, [i64, i64, i64, vp, vp, i64, vp, i64, vp]),
+        "tile_lu_apply_N": (i32, [i64, i64, i64, vp, vp, vp, i64, vp, i64, vp]),
         "tile_qr_t_elems": (sz, [i64, i64, i64]),
         "tile_lu_l_elems": (sz, [i64, i64, i64]),
         "tile_lu_ipiv_elems": (sz, [i64, i64]),
@@ -71,7 +78,8 @@ def _load():
 
 lib = _load()
 SYMBOLS = [
-    "tile_chol", "tile_qr", "tile_lu", "tile_qr_t_elems", "tile_lu_l_elems", "tile_lu_ipiv_elems",
+    "tile_chol", "tile_qr", "tile_lu", "tile_lu_nopiv", "tile_getrs", "tile_ormqr", "tile_qrs", "tile_lu_apply_N",
+    "tile_qr_t_elems", "tile_lu_l_elems", "tile_lu_ipiv_elems",
     "tile_pack", "tile_unpack", "tile_factor_host", "tile_set_policy", "tile_set_trace",
     "tile_trace_fetch", "tile_set_ctas", "tile_dag_export", "tk_run", "tile_dist_open",
     "tile_dist_ipc_bytes", "tile_dist_connect", "tile_dist_factor", "tile_dist_close",
@@ -139,6 +147,63 @@ def tile_lu(n, b, ib, A, Ls, ipiv, info=None, stream=None) -> None:
     _dev(ipiv, "ipiv", "int32", tile_lu_ipiv_elems(n, b))
     _info(info)
     _check(lib.tile_lu(n, b, ib, _ptr(A), _ptr(Ls), _ptr(ipiv), _ptr(info), _stream(stream)), "tile_lu")
+
+
+def tile_lu_nopiv(n, b, ib, A, Ls, ipiv, info=None, stream=None) -> None:
+    """GENP in tiled form (Algorithm 3 with every pivot kept)."""
+    _dev_f64(A, "A", n * n)
+    _dev_f64(Ls, "Ls", tile_lu_l_elems(n, b, ib))
+    _dev(ipiv, "ipiv", "int32", tile_lu_ipiv_elems(n, b))
+    _info(info)
+    _check(lib.tile_lu_nopiv(n, b, ib, _ptr(A), _ptr(Ls), _ptr(ipiv), _ptr(info), _stream(stream)), "tile_lu_nopiv")
+
+
+def _rhs(X, n):
+    """X: CUDA float64 tensor holding a column-major n x nrhs matrix: 1-D (nrhs = 1) or a
+    2-D tensor of shape (nrhs, n) (row-major storage of X^T = column-major X)."""
+    import torch
+    if X.dim() == 1:
+        _dev_f64(X, "X", n)
+        return 1, n
+    if X.dim() != 2 or X.shape[1] != n:
+        raise TileFactError("X must be 1-D of length n or 2-D of shape (nrhs, n) (column-major n x nrhs)")
+    _dev_f64(X, "X")
+    return X.shape[0], n
+
+
+def tile_getrs(n, b, ib, F, Ls, ipiv, X, stream=None) -> None:
+    """X <- A^{-1} X with the tile_lu factors (U^{-1} N^{-1} X, Eq. eq:GETWPcompact)."""
+    _dev_f64(F, "F", n * n)
+    _dev_f64(Ls, "Ls", tile_lu_l_elems(n, b, ib))
+    _dev(ipiv, "ipiv", "int32", tile_lu_ipiv_elems(n, b))
+    nrhs, ldx = _rhs(X, n)
+    _check(lib.tile_getrs(n, b, ib, _ptr(F), _ptr(Ls), _ptr(ipiv), nrhs, _ptr(X), ldx, _stream(stream)), "tile_getrs")
+
+
+def tile_lu_apply_N(n, b, ib, F, Ls, ipiv, X, stream=None) -> None:
+    """X <- N X (N of Eq. eq:formula N; apply to I for N explicitly)."""
+    _dev_f64(F, "F", n * n)
+    _dev_f64(Ls, "Ls", tile_lu_l_elems(n, b, ib))
+    _dev(ipiv, "ipiv", "int32", tile_lu_ipiv_elems(n, b))
+    nrhs, ldx = _rhs(X, n)
+    _check(lib.tile_lu_apply_N(n, b, ib, _ptr(F), _ptr(Ls), _ptr(ipiv), nrhs, _ptr(X), ldx, _stream(stream)),
+           "tile_lu_apply_N")
+
+
+def tile_ormqr(n, b, ib, F, T, X, stream=None) -> None:
+    """X <- Q^T X with the tile_qr factors."""
+    _dev_f64(F, "F", n * n)
+    _dev_f64(T, "T", tile_qr_t_elems(n, b, ib))
+    nrhs, ldx = _rhs(X, n)
+    _check(lib.tile_ormqr(n, b, ib, _ptr(F), _ptr(T), nrhs, _ptr(X), ldx, _stream(stream)), "tile_ormqr")
+
+
+def tile_qrs(n, b, ib, F, T, X, stream=None) -> None:
+    """X <- A^{-1} X = R^{-1} Q^T X with the tile_qr factors."""
+    _dev_f64(F, "F", n * n)
+    _dev_f64(T, "T", tile_qr_t_elems(n, b, ib))
+    nrhs, ldx = _rhs(X, n)
+    _check(lib.tile_qrs(n, b, ib, _ptr(F), _ptr(T), nrhs, _ptr(X), ldx, _stream(stream)), "tile_qrs")
 
 
 def tile_qr_t_elems(n, b, ib) -> int:

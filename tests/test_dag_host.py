@@ -14,6 +14,7 @@ import re
 
 import numpy as np
 import pytest
+import scipy.linalg
 
 import oracle
 import tilegen
@@ -252,7 +253,7 @@ def test_random_topological_replay_bitwise(alg):
 
 def test_library_exports_every_header_symbol():
     hdr = open(os.path.join(os.path.dirname(__file__), "..", "include", "tilefact.h")).read()
-    names = set(re.findall(r"^\s*(?:const\s+)?[A-Za-z_0-9]+\s*\*?\s+\**\s*(t[a-z_]+)\s*\(", hdr, re.M))
+    names = set(re.findall(r"^\s*(?:const\s+)?[A-Za-z_0-9]+\s*\*?\s+\**\s*(t[A-Za-z_]+)\s*\(", hdr, re.M))
     assert {"tile_chol", "tile_qr", "tile_lu", "tk_run", "tile_pack"} <= names
     for nm in names:
         assert hasattr(tf.lib, nm), nm
@@ -277,3 +278,108 @@ def test_flop_conventions():
     assert tf.lapack_flops("chol", 32768) == pytest.approx(1.1728e13, rel=1e-4)
     assert tf.lapack_flops("qr", 32768) == pytest.approx(4.6912e13, rel=1e-4)
     assert tf.true_flops("qr", 4096, 256, 32) / tf.lapack_flops("qr", 4096) == pytest.approx(1 + 32 / 1024)
+
+
+# ------------------------------------------------------------------ solve / apply DAGs (NEXT-3)
+
+def _solve_task(alg, F, S, piv, Xt, p, b, ib, task):
+    """One solve-DAG task on the right-hand-side tiles Xt[i] (b x b, Fortran), with the
+    oracle's tile kernels for the factorization's own update steps and the textbook
+    operations (C4 of SURVEY §8(c)) for the rest."""
+    kind, k, i, c = task
+    bb = b * b
+    T = lambda r, q: F[(r + q * p) * bb:(r + q * p + 1) * bb].reshape(b, b).T  # noqa: E731
+
+    def Sv(r, q):
+        o = (r + q * p) * ib * b
+        return np.asfortranarray(S[o:o + ib * b].reshape(b, ib).T)
+
+    PV = lambda r, q: np.ascontiguousarray(piv[(r + q * p) * b:(r + q * p + 1) * b])  # noqa: E731
+    SK = tf.SOLVE_KINDS
+    if kind == SK["unitl"]:
+        return
+    if kind == SK["xgessm"]:
+        oracle.gessm(T(k, k), PV(k, k), Xt[k], ib)
+    elif kind == SK["xssssm"]:
+        oracle.ssssm(T(i, k), Sv(i, k), PV(i, k), Xt[k], Xt[i], ib)
+    elif kind == SK["xlarfb"]:
+        oracle.larfb(T(k, k), Sv(k, k), Xt[k], ib)
+    elif kind == SK["xssrfb"]:
+        oracle.ssrfb(T(i, k), Sv(i, k), Xt[k], Xt[i], ib)
+    elif kind == SK["xtrsmu"]:
+        Xt[k][:] = scipy.linalg.solve_triangular(np.triu(T(k, k)), Xt[k])
+    elif kind == SK["xgemm"]:
+        Xt[i][:] = Xt[i] - T(i, k) @ Xt[k]
+    elif kind == SK["xunssssm"]:
+        L, Ls, pv = T(i, k), Sv(i, k), PV(i, k)
+        for s in range(b // ib - 1, -1, -1):
+            c0, c1 = s * ib, (s + 1) * ib
+            x1 = Xt[k][c0:c1].copy()
+            Xt[i][:] = Xt[i] + L[:, c0:c1] @ x1
+            Xt[k][c0:c1] = x1 + np.tril(Ls[:, c0:c1], -1) @ x1
+            for j in range(c1 - 1, c0 - 1, -1):
+                if pv[j] > b:
+                    r = pv[j] - b - 1
+                    Xt[k][j], Xt[i][r] = Xt[i][r].copy(), Xt[k][j].copy()
+    elif kind == SK["xungessm"]:
+        Xt[k][:] = Xt[k] + np.tril(T(k, k), -1) @ Xt[k]
+        pv = PV(k, k)
+        for j in range(b - 1, -1, -1):
+            r = pv[j] - 1
+            if r != j:
+                Xt[k][[j, r]] = Xt[k][[r, j]]
+
+
+@pytest.mark.parametrize("alg", ["getrs", "ormqr", "qrs", "lu_apply_N"])
+def test_solve_dag_random_replay(alg):
+    """Dependency soundness of the solve DAGs: random topological orders of the exported
+    graph reproduce the program-order result bitwise, and that result is the oracle's
+    solve / Q^T / N application (to rounding)."""
+    n, b, ib, p = 48, 12, 4, 4
+    lu = alg in ("getrs", "lu_apply_N")
+    A = (tilegen.normal if lu else tilegen.uniform)(n, 5)
+    F = oracle.pack(A, b)
+    if lu:
+        S, piv, _ = oracle.lu(F, n, b, ib)
+    else:
+        S, piv = oracle.qr(F, n, b, ib), np.zeros(1, dtype=np.int32)
+    Y = np.asfortranarray(tilegen.normal(n, 6)[:, :b])
+    d = tf.tile_dag_export(alg, p)
+    tasks = _tasks(d)
+    pr = _preds(d)
+    assert all(t[0] >= 14 for t in tasks)
+
+    def run(order):
+        Xt = [np.asfortranarray(Y[r * b:(r + 1) * b].copy()) for r in range(p)]
+        for t in order:
+            _solve_task(alg, F, S, piv, Xt, p, b, ib, tasks[t])
+        return np.vstack(Xt)
+
+    ref = run(range(len(tasks)))
+    rng = np.random.default_rng(1)
+    for _ in range(4):
+        indeg = [len(x) for x in pr]
+        succ = [[] for _ in tasks]
+        for t, ps in enumerate(pr):
+            for x in ps:
+                succ[x].append(t)
+        ready = [t for t in range(len(tasks)) if indeg[t] == 0]
+        order = []
+        while ready:
+            t = ready.pop(int(rng.integers(len(ready))))
+            order.append(t)
+            for s_ in succ[t]:
+                indeg[s_] -= 1
+                if indeg[s_] == 0:
+                    ready.append(s_)
+        assert len(order) == len(tasks)
+        assert np.array_equal(run(order), ref)
+    if alg == "getrs":
+        want = oracle.lu_solve(F, S, piv, Y, n, b, ib)
+    elif alg == "lu_apply_N":
+        want = oracle.lu_apply_N(F, S, piv, Y, n, b, ib)
+    elif alg == "ormqr":
+        want = oracle.qr_apply(F, S, Y, n, b, ib, trans=True)
+    else:
+        want = oracle.qr_solve(F, S, Y, n, b, ib)
+    assert np.max(np.abs(ref - want)) <= 1e-10 * max(1.0, np.max(np.abs(want)))

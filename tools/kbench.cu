@@ -22,6 +22,7 @@ kb_kernel(int kind, int b, int ib, double* tiles, double* aux, int* ipiv, double
   extern __shared__ __align__(16) double sm[];
   Ctx cx;
   cx.b = b; cx.ib = ib; cx.scratch = scratch + (size_t)blockIdx.x * scr; cx.info = nullptr; cx.abort_flag = nullptr;
+  cx.nopiv = 0;
   const size_t bb = (size_t)b * b;
   double* t0 = tiles + (size_t)blockIdx.x * 3 * bb;
   double* t1 = t0 + bb;

@@ -108,6 +108,18 @@ int tile_qrs(int64_t n, int64_t b, int64_t ib, const double* dF, const double* d
 int tile_lu_apply_N(int64_t n, int64_t b, int64_t ib, const double* dF, const double* dLs,
                     const int32_t* dIpiv, int64_t nrhs, double* dX, int64_t ldx, tf_stream_t stream);
 
+/* Rectangular tiled QR / LU: Algorithm 2 / 3 on an m x n matrix of
+ * p x q tiles, p = m/b, q = n/b ("p-by-q tiled matrix", 548-557), panels
+ * k < min(p, q).  BDL with p tile rows: tile (i,j) at (i + j*p)*b*b.  T / L strips (i,k)
+ * at (i + k*p)*ib*b and pivot vectors (i,k) at (i + k*p)*b for k < min(p, q): sizes
+ * tile_mn_aux_elems / tile_mn_ipiv_elems.  Otherwise as tile_qr / tile_lu (m = n is the
+ * square call). */
+int tile_qr_mn(int64_t m, int64_t n, int64_t b, int64_t ib, double* dA, double* dT, tf_stream_t stream);
+int tile_lu_mn(int64_t m, int64_t n, int64_t b, int64_t ib, double* dA, double* dLs, int32_t* dIpiv,
+               int32_t* d_info, tf_stream_t stream);
+size_t tile_mn_aux_elems(int64_t m, int64_t n, int64_t b, int64_t ib);  /* p*min(p,q)*ib*b */
+size_t tile_mn_ipiv_elems(int64_t m, int64_t n, int64_t b);             /* p*min(p,q)*b */
+
 size_t tile_qr_t_elems(int64_t n, int64_t b, int64_t ib);  /* p*p*ib*b */
 size_t tile_lu_l_elems(int64_t n, int64_t b, int64_t ib);  /* p*p*ib*b */
 size_t tile_lu_ipiv_elems(int64_t n, int64_t b);           /* p*p*b */

@@ -72,6 +72,10 @@ def lib():
             "o_chol_residual": (ctypes.c_double, [i64, dp, dp]),
             "o_kernel_flops": (ctypes.c_double, [ctypes.c_int, ctypes.c_double, ctypes.c_double]),
             "o_decisions_arm": (None, [dp, i64]),
+            "o_qr_mn": (None, [i64, i64, i64, i64, dp, dp]),
+            "o_lu_mn": (ctypes.c_int, [i64, i64, i64, i64, dp, dp, ip]),
+            "o_qr_apply_mn": (None, [i64, i64, i64, i64, dp, dp, dp, i64, ctypes.c_int]),
+            "o_lu_apply_N_mn": (None, [i64, i64, i64, i64, dp, dp, ip, dp, i64]),
             "o_lu_nopiv": (ctypes.c_int, [i64, i64, i64, dp, dp, ip]),
             "o_ref_genp": (ctypes.c_int, [i64, dp]),
             "o_trsm_upper_bdl": (None, [i64, i64, dp, dp, i64, i64]),
@@ -197,6 +201,47 @@ def lu(tiles: np.ndarray, n: int, b: int, ib: int):
     piv = np.zeros(p * p * b, dtype=np.int32)
     info = lib().o_lu(n, b, ib, _d(tiles), _d(Ls), _i(piv))
     return Ls, piv, info
+
+
+# ---------------------------------------------------------------- rectangular (NEXT-4)
+
+def qr_mn(tiles: np.ndarray, m: int, n: int, b: int, ib: int) -> np.ndarray:
+    """Algorithm 2 on an m x n matrix (p x q tiles).  Returns T strips
+    (p * min(p, q) strips of ib x b)."""
+    p, q = m // b, n // b
+    T = np.zeros(p * min(p, q) * ib * b, dtype=np.float64)
+    lib().o_qr_mn(m, n, b, ib, _d(tiles), _d(T))
+    return T
+
+
+def lu_mn(tiles: np.ndarray, m: int, n: int, b: int, ib: int):
+    """Algorithm 3 on an m x n matrix (p x q tiles)."""
+    p, q = m // b, n // b
+    Ls = np.zeros(p * min(p, q) * ib * b, dtype=np.float64)
+    piv = np.zeros(p * min(p, q) * b, dtype=np.int32)
+    info = lib().o_lu_mn(m, n, b, ib, _d(tiles), _d(Ls), _i(piv))
+    return Ls, piv, info
+
+
+def qr_apply_mn(F, T, X, m, n, b, ib, trans=False):
+    X = np.asfortranarray(X, dtype=np.float64).copy(order="F")
+    X = X.reshape(-1, 1, order="F") if X.ndim == 1 else X
+    lib().o_qr_apply_mn(m, n, b, ib, _d(np.ascontiguousarray(F)), _d(np.ascontiguousarray(T)), _d(X),
+                        X.shape[1], 1 if trans else 0)
+    return X
+
+
+def lu_apply_N_mn(F, Ls, piv, X, m, n, b, ib):
+    X = np.asfortranarray(X, dtype=np.float64).copy(order="F")
+    X = X.reshape(-1, 1, order="F") if X.ndim == 1 else X
+    lib().o_lu_apply_N_mn(m, n, b, ib, _d(np.ascontiguousarray(F)), _d(np.ascontiguousarray(Ls)),
+                          _i(np.ascontiguousarray(piv)), _d(X), X.shape[1])
+    return X
+
+
+def upper_mn(F, m, n, b):
+    """R / U of an m x n factorization: the upper trapezoid of the unpacked matrix."""
+    return np.triu(unpack(F, m, n, b))
 
 
 def lu_nopiv(tiles: np.ndarray, n: int, b: int, ib: int):

@@ -321,46 +321,57 @@ void o_ssrfb(int64_t b, int64_t ib, const double* V, const double* Tst, double* 
 }
 
 /* Algorithm 2, square p x p tiles, in program order. */
-void o_qr(int64_t n, int64_t b, int64_t ib, double* A, double* T) {
-  int64_t p = n / b;
-  for (int64_t k = 0; k < p; ++k) {
+/* Algorithm 2 on an m x n matrix of p x q tiles ("the tiled QR of
+ * a p-by-q tiled matrix"), k < min(p, q).  T strips (i,k) at (i + k*p)*ib*b. */
+void o_qr_mn(int64_t m, int64_t n, int64_t b, int64_t ib, double* A, double* T) {
+  int64_t p = m / b, q = n / b, kk = p < q ? p : q;
+  for (int64_t k = 0; k < kk; ++k) {
     o_geqrt(b, ib, OT(A, p, b, k, k), OSTRIP(T, p, b, ib, k, k));
-    for (int64_t j = k + 1; j < p; ++j)
+    for (int64_t j = k + 1; j < q; ++j)
       o_larfb(b, ib, OT(A, p, b, k, k), OSTRIP(T, p, b, ib, k, k), OT(A, p, b, k, j));
     for (int64_t i = k + 1; i < p; ++i) {
       o_tsqrt(b, ib, OT(A, p, b, k, k), OT(A, p, b, i, k), OSTRIP(T, p, b, ib, i, k));
-      for (int64_t j = k + 1; j < p; ++j)
+      for (int64_t j = k + 1; j < q; ++j)
         o_ssrfb(b, ib, OT(A, p, b, i, k), OSTRIP(T, p, b, ib, i, k), OT(A, p, b, k, j), OT(A, p, b, i, j));
     }
   }
 }
 
+/* Algorithm 2, square p x p tiles, program order. */
+void o_qr(int64_t n, int64_t b, int64_t ib, double* A, double* T) { o_qr_mn(n, n, b, ib, A, T); }
+
 /* C4: X (n x ncol, column-major, ld n) <- Q X (trans == 0) or Q^T X (trans != 0),
  * Q the orthogonal factor held implicitly by the factored tiles and T strips.
  * Q X applies the inverses of the factorization's block reflectors in reverse task
  * order and reverse inner-block order, with T untransposed. */
-void o_qr_apply(int64_t n, int64_t b, int64_t ib, const double* F, const double* T, double* X,
-                int64_t ncol, int trans) {
-  int64_t p = n / b, t = b / ib;
+void o_qr_apply_mn(int64_t m, int64_t n, int64_t b, int64_t ib, const double* F, const double* T, double* X,
+                   int64_t ncol, int trans) {
+  /* m x n factors (p x q tiles): Q is m x m, X is m x ncol (ld m) */
+  int64_t p = m / b, q = n / b, t = b / ib, kk = p < q ? p : q;
   if (trans) {
-    for (int64_t k = 0; k < p; ++k) {
+    for (int64_t k = 0; k < kk; ++k) {
       for (int64_t s = 0; s < t; ++s)
-        o_apply_geq_block(b, ib, s, OT(F, p, b, k, k), OSTRIP(T, p, b, ib, k, k), X + k * b, n, ncol, 1);
+        o_apply_geq_block(b, ib, s, OT(F, p, b, k, k), OSTRIP(T, p, b, ib, k, k), X + k * b, m, ncol, 1);
       for (int64_t i = k + 1; i < p; ++i)
         for (int64_t s = 0; s < t; ++s)
-          o_apply_ts_block(b, ib, s, OT(F, p, b, i, k), OSTRIP(T, p, b, ib, i, k), X + k * b, n,
-                           X + i * b, n, ncol, 1);
+          o_apply_ts_block(b, ib, s, OT(F, p, b, i, k), OSTRIP(T, p, b, ib, i, k), X + k * b, m,
+                           X + i * b, m, ncol, 1);
     }
   } else {
-    for (int64_t k = p - 1; k >= 0; --k) {
+    for (int64_t k = kk - 1; k >= 0; --k) {
       for (int64_t i = p - 1; i > k; --i)
         for (int64_t s = t - 1; s >= 0; --s)
-          o_apply_ts_block(b, ib, s, OT(F, p, b, i, k), OSTRIP(T, p, b, ib, i, k), X + k * b, n,
-                           X + i * b, n, ncol, 0);
+          o_apply_ts_block(b, ib, s, OT(F, p, b, i, k), OSTRIP(T, p, b, ib, i, k), X + k * b, m,
+                           X + i * b, m, ncol, 0);
       for (int64_t s = t - 1; s >= 0; --s)
-        o_apply_geq_block(b, ib, s, OT(F, p, b, k, k), OSTRIP(T, p, b, ib, k, k), X + k * b, n, ncol, 0);
+        o_apply_geq_block(b, ib, s, OT(F, p, b, k, k), OSTRIP(T, p, b, ib, k, k), X + k * b, m, ncol, 0);
     }
   }
+}
+
+void o_qr_apply(int64_t n, int64_t b, int64_t ib, const double* F, const double* T, double* X,
+                int64_t ncol, int trans) {
+  o_qr_apply_mn(n, n, b, ib, F, T, X, ncol, trans);
 }
 
 /* ====================================================================================
@@ -555,26 +566,31 @@ void o_ssssm(int64_t b, int64_t ib, const double* L, const double* Ls, const int
 
 /* Algorithm 3, square p x p tiles, program order.  Returns 0 or the
  * smallest global column (1-based) whose pivot was exactly zero. */
-int o_lu(int64_t n, int64_t b, int64_t ib, double* A, double* Ls, int32_t* ipiv) {
-  int64_t p = n / b;
+int o_lu_mn(int64_t m, int64_t n, int64_t b, int64_t ib, double* A, double* Ls, int32_t* ipiv) {
+  /* Algorithm 3 on an m x n matrix of p x q tiles, k < min(p, q) */
+  int64_t p = m / b, q = n / b, kk = p < q ? p : q;
   int64_t best = 0;
-  for (int64_t k = 0; k < p; ++k) {
+  for (int64_t k = 0; k < kk; ++k) {
     int info = 0;
     o_getrf(b, ib, OT(A, p, b, k, k), OPIV(ipiv, p, b, k, k), &info);
     if (info && (best == 0 || k * b + info < best)) best = k * b + info;
-    for (int64_t j = k + 1; j < p; ++j)
+    for (int64_t j = k + 1; j < q; ++j)
       o_gessm(b, ib, OT(A, p, b, k, k), OPIV(ipiv, p, b, k, k), OT(A, p, b, k, j));
     for (int64_t i = k + 1; i < p; ++i) {
       info = 0;
       o_tstrf(b, ib, OT(A, p, b, k, k), OT(A, p, b, i, k), OSTRIP(Ls, p, b, ib, i, k),
               OPIV(ipiv, p, b, i, k), &info);
       if (info && (best == 0 || k * b + info < best)) best = k * b + info;
-      for (int64_t j = k + 1; j < p; ++j)
+      for (int64_t j = k + 1; j < q; ++j)
         o_ssssm(b, ib, OT(A, p, b, i, k), OSTRIP(Ls, p, b, ib, i, k), OPIV(ipiv, p, b, i, k),
                 OT(A, p, b, k, j), OT(A, p, b, i, j));
     }
   }
   return (int)best;
+}
+
+int o_lu(int64_t n, int64_t b, int64_t ib, double* A, double* Ls, int32_t* ipiv) {
+  return o_lu_mn(n, n, b, ib, A, Ls, ipiv);
 }
 
 /* GENP in tiled form: Algorithm 3 with every pivot kept (o_nopiv).
@@ -664,10 +680,12 @@ void o_lu_solve(int64_t n, int64_t b, int64_t ib, const double* F, const double*
 /* C4 / Eq. (eq:formula N), (eq:GETWPcompact):
  * X (n x ncol, ld n) <- N X, N = (prod of the elementary L and P of GETWP)^{-1},
  * applied implicitly by undoing every elimination step in reverse program order. */
-void o_lu_apply_N(int64_t n, int64_t b, int64_t ib, const double* F, const double* Ls,
-                  const int32_t* ipiv, double* X, int64_t ncol) {
-  int64_t p = n / b, t = b / ib;
-  for (int64_t k = p - 1; k >= 0; --k) {
+void o_lu_apply_N_mn(int64_t m, int64_t n, int64_t b, int64_t ib, const double* F, const double* Ls,
+                     const int32_t* ipiv, double* X, int64_t ncol) {
+  /* m x n factors (p x q tiles): N is m x m, X is m x ncol (ld m) */
+  int64_t p = m / b, q = n / b, t = b / ib, kk = p < q ? p : q;
+  const int64_t ldn = m;
+  for (int64_t k = kk - 1; k >= 0; --k) {
     double* x1 = X + k * b;
     for (int64_t i = p - 1; i > k; --i) {
       const double* L = OT(F, p, b, i, k);
@@ -680,21 +698,21 @@ void o_lu_apply_N(int64_t n, int64_t b, int64_t ib, const double* F, const doubl
           /* x2 += L[:, c0:c1] x1[c0:c1] (uses x1 before its update) */
           for (int64_t r = 0; r < b; ++r) {
             double acc = 0.0;
-            for (int64_t m = c0; m < c1; ++m) acc += OE(L, b, r, m) * OE(x1, n, m, c);
-            OE(x2, n, r, c) += acc;
+            for (int64_t m = c0; m < c1; ++m) acc += OE(L, b, r, m) * OE(x1, ldn, m, c);
+            OE(x2, ldn, r, c) += acc;
           }
           /* x1[c0:c1] <- (I + Ls_s) x1[c0:c1]; rows descending so inputs stay original */
           for (int64_t r = c1 - 1; r >= c0; --r) {
             double acc = 0.0;
-            for (int64_t m = c0; m < r; ++m) acc += OE(Lst, ib, r - c0, m) * OE(x1, n, m, c);
-            OE(x1, n, r, c) += acc;
+            for (int64_t m = c0; m < r; ++m) acc += OE(Lst, ib, r - c0, m) * OE(x1, ldn, m, c);
+            OE(x1, ldn, r, c) += acc;
           }
         }
         for (int64_t j = c1 - 1; j >= c0; --j)
           if (pv[j] > b) {
             int64_t r = pv[j] - b - 1;
             for (int64_t c = 0; c < ncol; ++c) {
-              double tmp = OE(x1, n, j, c); OE(x1, n, j, c) = OE(x2, n, r, c); OE(x2, n, r, c) = tmp;
+              double tmp = OE(x1, ldn, j, c); OE(x1, ldn, j, c) = OE(x2, ldn, r, c); OE(x2, ldn, r, c) = tmp;
             }
           }
       }
@@ -705,17 +723,22 @@ void o_lu_apply_N(int64_t n, int64_t b, int64_t ib, const double* F, const doubl
     for (int64_t c = 0; c < ncol; ++c)
       for (int64_t r = b - 1; r >= 0; --r) {
         double acc = 0.0;
-        for (int64_t m = 0; m < r; ++m) acc += OE(Lkk, b, r, m) * OE(x1, n, m, c);
-        OE(x1, n, r, c) += acc;
+        for (int64_t m = 0; m < r; ++m) acc += OE(Lkk, b, r, m) * OE(x1, ldn, m, c);
+        OE(x1, ldn, r, c) += acc;
       }
     for (int64_t j = b - 1; j >= 0; --j) {
       int64_t r = pv[j] - 1;
       if (r != j)
         for (int64_t c = 0; c < ncol; ++c) {
-          double tmp = OE(x1, n, j, c); OE(x1, n, j, c) = OE(x1, n, r, c); OE(x1, n, r, c) = tmp;
+          double tmp = OE(x1, ldn, j, c); OE(x1, ldn, j, c) = OE(x1, ldn, r, c); OE(x1, ldn, r, c) = tmp;
         }
     }
   }
+}
+
+void o_lu_apply_N(int64_t n, int64_t b, int64_t ib, const double* F, const double* Ls,
+                  const int32_t* ipiv, double* X, int64_t ncol) {
+  o_lu_apply_N_mn(n, n, b, ib, F, Ls, ipiv, X, ncol);
 }
 
 /* ====================================================================================

@@ -84,8 +84,11 @@ int level_of(int kind, int k, int j, int policy) {
 }
 
 // Tasks of Algorithms 1-3 in program order and their predecessor lists (a13 rules).
+// qc: tile columns (QR / LU on a p x qc tiled matrix; k < min(p, qc));
+// < 0 = square.
 void global_tasks(int alg, int p, int b, int ib, int policy, std::vector<TaskD>& tasks,
-                  std::vector<std::vector<int>>& preds) {
+                  std::vector<std::vector<int>>& preds, int qc = -1) {
+  if (qc < 0) qc = p;
   std::unordered_map<uint64_t, int> id;
   id.reserve((size_t)p * p * p / 2 + 16);
   tasks.clear();
@@ -103,12 +106,13 @@ void global_tasks(int alg, int p, int b, int ib, int policy, std::vector<TaskD>&
     }
   } else {
     const int F = alg == 1 ? 4 : 8, R = F + 1, C = F + 2, U = F + 3;
-    for (int k = 0; k < p; ++k) {
+    const int kk = p < qc ? p : qc;
+    for (int k = 0; k < kk; ++k) {
       add(F, k, k, k);
-      for (int j = k + 1; j < p; ++j) add(R, k, k, j);
+      for (int j = k + 1; j < qc; ++j) add(R, k, k, j);
       for (int i = k + 1; i < p; ++i) {
         add(C, k, i, k);
-        for (int j = k + 1; j < p; ++j) add(U, k, i, j);
+        for (int j = k + 1; j < qc; ++j) add(U, k, i, j);
       }
     }
   }
@@ -249,11 +253,11 @@ void finalize_dag(HostDag& G, const std::vector<std::vector<int>>& preds) {
     if (G.indeg0[t] == 0 && G.tasks[t].kind != K_RECV) G.roots.push_back(t);
 }
 
-void build_dag(HostDag& G, int alg, int p, int b, int ib, int policy, int q = 0) {
+void build_dag(HostDag& G, int alg, int p, int b, int ib, int policy, int q = 0, int qc = -1) {
   G.alg = alg; G.p = p; G.b = b; G.policy = policy;
   std::vector<std::vector<int>> preds;
   if (alg >= ALG_GETRS) solve_tasks(alg, p, b, ib, q, policy, G.tasks, preds);
-  else global_tasks(alg, p, b, ib, policy, G.tasks, preds);
+  else global_tasks(alg, p, b, ib, policy, G.tasks, preds, qc);
   finalize_dag(G, preds);
 }
 
@@ -382,7 +386,7 @@ struct DevDag {
   SendEnt* sends = nullptr;
 };
 
-std::map<std::tuple<int, int, int, int, int, int, int>, DevDag> g_dags;  // (dev, alg, p, b, ib, policy, q)
+std::map<std::tuple<int, int, int, int, int, int, int, int>, DevDag> g_dags;  // (dev, alg, p, b, ib, policy, q, qc)
 
 template <class T>
 int upload(T** dst, const std::vector<T>& v) {
@@ -413,13 +417,13 @@ void free_dag(DevDag& D) {
   D = DevDag();
 }
 
-int get_dag(int dev, int alg, int p, int b, int ib, DevDag** out, int q = 0) {
-  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy, q);
+int get_dag(int dev, int alg, int p, int b, int ib, DevDag** out, int q = 0, int qc = -1) {
+  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy, q, qc);
   auto it = g_dags.find(key);
   if (it != g_dags.end()) { *out = &it->second; return 0; }
   DevDag D;
   D.h = std::make_shared<HostDag>();
-  build_dag(*D.h, alg, p, b, ib, g_policy, q);
+  build_dag(*D.h, alg, p, b, ib, g_policy, q, qc);
   int rc;
   if ((rc = upload_dag(D))) return rc;
   auto res = g_dags.emplace(key, D);
@@ -518,16 +522,19 @@ long long watchdog_ns() {
   return s > 0 ? (long long)(s * 1e9) : 0;
 }
 
+// m_rows >= 0: QR / LU of an m_rows x n matrix (p = m_rows/b tile rows, n/b tile columns).
 int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, double* aux, int32_t* ipiv,
-                      int32_t* d_info, cudaStream_t stream, double* X = nullptr, int q = 0, int nopiv = 0) {
+                      int32_t* d_info, cudaStream_t stream, double* X = nullptr, int q = 0, int nopiv = 0,
+                      int64_t m_rows = -1) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   int dev;
   TF_CUDA(cudaGetDevice(&dev));
   int rc;
   if ((rc = device_setup(dev))) return rc;
-  const int p = (int)(n / b);
+  const int p = (int)((m_rows >= 0 ? m_rows : n) / b);
+  const int qc = m_rows >= 0 ? (int)(n / b) : -1;
   DevDag* D;
-  if ((rc = get_dag(dev, alg, p, (int)b, (int)ib, &D, q))) return rc;
+  if ((rc = get_dag(dev, alg, p, (int)b, (int)ib, &D, q, qc))) return rc;
   const HostDag& H = *D->h;
   Workspace& W = g_ws[std::make_pair(dev, stream)];
   W.stream = stream;
@@ -857,6 +864,41 @@ int tile_lu_nopiv(int64_t n, int64_t b, int64_t ib, double* dA, double* dLs, int
   if (!dLs) { set_err("null L-strip pointer"); return -5; }
   if (!dIpiv) { set_err("null ipiv pointer"); return -6; }
   return run_factorization(2, n, b, ib, dA, dLs, dIpiv, d_info, (cudaStream_t)stream, nullptr, 0, 1);
+}
+
+// Rectangular QR / LU (NEXT-4).
+static int check_mn(int64_t m, int64_t n, int64_t b, int64_t ib, const void* dA) {
+  if (m <= 0) { set_err("m must be > 0"); return -1; }
+  if (n <= 0) { set_err("n must be > 0"); return -2; }
+  if (b <= 0 || m % b || n % b || b > TF_MAX_B) { set_err("b must be > 0 and divide m and n"); return -3; }
+  if (ib <= 0 || b % ib) { set_err("ib must be > 0 and divide b"); return -4; }
+  if (!dA) { set_err("null matrix pointer"); return -5; }
+  if ((m / b) * (n / b) > (int64_t)1 << 24) { set_err("too many tiles"); return -1; }
+  return 0;
+}
+int tile_qr_mn(int64_t m, int64_t n, int64_t b, int64_t ib, double* dA, double* dT, tf_stream_t stream) {
+  int rc = check_mn(m, n, b, ib, dA);
+  if (rc) return rc;
+  if (!dT) { set_err("null T pointer"); return -6; }
+  return run_factorization(1, n, b, ib, dA, dT, nullptr, nullptr, (cudaStream_t)stream, nullptr, 0, 0, m);
+}
+int tile_lu_mn(int64_t m, int64_t n, int64_t b, int64_t ib, double* dA, double* dLs, int32_t* dIpiv,
+               int32_t* d_info, tf_stream_t stream) {
+  int rc = check_mn(m, n, b, ib, dA);
+  if (rc) return rc;
+  if (!dLs) { set_err("null L-strip pointer"); return -6; }
+  if (!dIpiv) { set_err("null ipiv pointer"); return -7; }
+  return run_factorization(2, n, b, ib, dA, dLs, dIpiv, d_info, (cudaStream_t)stream, nullptr, 0, 0, m);
+}
+size_t tile_mn_aux_elems(int64_t m, int64_t n, int64_t b, int64_t ib) {
+  if (m <= 0 || n <= 0 || b <= 0 || m % b || n % b) return 0;
+  const size_t p = m / b, q = n / b;
+  return p * (p < q ? p : q) * (size_t)ib * b;
+}
+size_t tile_mn_ipiv_elems(int64_t m, int64_t n, int64_t b) {
+  if (m <= 0 || n <= 0 || b <= 0 || m % b || n % b) return 0;
+  const size_t p = m / b, q = n / b;
+  return p * (p < q ? p : q) * (size_t)b;
 }
 
 size_t tile_qr_t_elems(int64_t n, int64_t b, int64_t ib) {

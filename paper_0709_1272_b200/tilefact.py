@@ -41,6 +41,10 @@ def _load():
         "tile_ormqr": (i32, [i64, i64, i64, vp, vp, i64, vp, i64, vp]),
         "tile_qrs": (i32, [i64, i64, i64, vp, vp, i64, vp, i64, vp]),
         "tile_lu_apply_N": (i32, [i64, i64, i64, vp, vp, vp, i64, vp, i64, vp]),
+        "tile_qr_mn": (i32, [i64, i64, i64, i64, vp, vp, vp]),
+        "tile_lu_mn": (i32, [i64, i64, i64, i64, vp, vp, vp, vp, vp]),
+        "tile_mn_aux_elems": (sz, [i64, i64, i64, i64]),
+        "tile_mn_ipiv_elems": (sz, [i64, i64, i64]),
         "tile_qr_t_elems": (sz, [i64, i64, i64]),
         "tile_lu_l_elems": (sz, [i64, i64, i64]),
         "tile_lu_ipiv_elems": (sz, [i64, i64]),
@@ -78,7 +82,8 @@ def _load():
 
 lib = _load()
 SYMBOLS = [
-    "tile_chol", "tile_qr", "tile_lu", "tile_lu_nopiv", "tile_getrs", "tile_ormqr", "tile_qrs", "tile_lu_apply_N",
+    "tile_chol", "tile_qr", "tile_lu", "tile_qr_mn", "tile_lu_mn", "tile_mn_aux_elems", "tile_mn_ipiv_elems",
+    "tile_lu_nopiv", "tile_getrs", "tile_ormqr", "tile_qrs", "tile_lu_apply_N",
     "tile_qr_t_elems", "tile_lu_l_elems", "tile_lu_ipiv_elems",
     "tile_pack", "tile_unpack", "tile_factor_host", "tile_set_policy", "tile_set_trace",
     "tile_trace_fetch", "tile_set_ctas", "tile_dag_export", "tk_run", "tile_dist_open",
@@ -204,6 +209,30 @@ def tile_qrs(n, b, ib, F, T, X, stream=None) -> None:
     _dev_f64(T, "T", tile_qr_t_elems(n, b, ib))
     nrhs, ldx = _rhs(X, n)
     _check(lib.tile_qrs(n, b, ib, _ptr(F), _ptr(T), nrhs, _ptr(X), ldx, _stream(stream)), "tile_qrs")
+
+
+def tile_mn_aux_elems(m, n, b, ib) -> int:
+    return int(lib.tile_mn_aux_elems(m, n, b, ib))
+
+
+def tile_mn_ipiv_elems(m, n, b) -> int:
+    return int(lib.tile_mn_ipiv_elems(m, n, b))
+
+
+def tile_qr_mn(m, n, b, ib, A, T, stream=None) -> None:
+    """Tiled QR of an m x n BDL matrix (p x q tiles)."""
+    _dev_f64(A, "A", m * n)
+    _dev_f64(T, "T", tile_mn_aux_elems(m, n, b, ib))
+    _check(lib.tile_qr_mn(m, n, b, ib, _ptr(A), _ptr(T), _stream(stream)), "tile_qr_mn")
+
+
+def tile_lu_mn(m, n, b, ib, A, Ls, ipiv, info=None, stream=None) -> None:
+    """Tiled LU with incremental pivoting of an m x n BDL matrix."""
+    _dev_f64(A, "A", m * n)
+    _dev_f64(Ls, "Ls", tile_mn_aux_elems(m, n, b, ib))
+    _dev(ipiv, "ipiv", "int32", tile_mn_ipiv_elems(m, n, b))
+    _info(info)
+    _check(lib.tile_lu_mn(m, n, b, ib, _ptr(A), _ptr(Ls), _ptr(ipiv), _ptr(info), _stream(stream)), "tile_lu_mn")
 
 
 def tile_qr_t_elems(n, b, ib) -> int:

@@ -422,7 +422,10 @@ def run_ours(args, rank, world, local_rank):
         torch.distributed.barrier()
     from paper_0709_1272_b200 import tilefact as tf
     torch.cuda.set_device(local_rank)
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.weak and world > 1:
+        cfg["n"] = cfg["b"] * round(cfg["n"] * world ** 0.5 / cfg["b"])
+        cfg["desc"] = cfg["desc"] + f" (weak scaling: n scaled by sqrt({world}) to {cfg['n']})"
     n, b, ib = cfg["n"], cfg["b"], cfg["ib"]
     peak_sus, peak_burst, peak_src = fp64_peak()
     launches_per_step = 3  # reset, seed, persistent scheduler kernel (per rank)
@@ -497,7 +500,7 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": round(gflops, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded; BASELINE recipe generated on device)",
             "config": {"workload": cfg["desc"], "n": n, "b": b, "ib": ib, "grid": grid,
                        "parallelism": "1 GPU" if world == 1 else
@@ -535,6 +538,9 @@ def main():
     ap.add_argument("--only", action="store_true", help="skip the per-factorization table")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: n = n_config * sqrt(N) rounded to a multiple of b (fixed memory per GPU, "
+                         "the paper's nloc convention PAPER.md:1112-1114); reports scaling 'weak'")
     args = ap.parse_args()
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
         # launched as `python bench.py --gpus N`: start the N ranks ourselves (one process

@@ -31,7 +31,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-                               "-shared", "-std=c11", "-o", tmp, _SRC, "-lm"])
+                               "-shared", "-std=c11", "-o", tmp, _SRC, "-lm", "-lpthread"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -72,6 +72,7 @@ def lib():
             "o_chol_residual": (ctypes.c_double, [i64, dp, dp]),
             "o_kernel_flops": (ctypes.c_double, [ctypes.c_int, ctypes.c_double, ctypes.c_double]),
             "o_decisions_arm": (None, [dp, i64]),
+            "o_factor_par": (ctypes.c_int, [ctypes.c_int, i64, i64, i64, dp, dp, ip, ctypes.c_int]),
             "o_qr_mn": (None, [i64, i64, i64, i64, dp, dp]),
             "o_lu_mn": (ctypes.c_int, [i64, i64, i64, i64, dp, dp, ip]),
             "o_qr_apply_mn": (None, [i64, i64, i64, i64, dp, dp, dp, i64, ctypes.c_int]),
@@ -283,6 +284,18 @@ def lu_solve(F, Ls, piv, X, n, b, ib):
 def qr_solve(F, T, X, n, b, ib):
     """X <- A^{-1} X = R^{-1} Q^T X with the factors of Algorithm 2."""
     return trsm_upper(F, qr_apply(F, T, X, n, b, ib, trans=True), n, b)
+
+
+def factor_par(alg: str, tiles: np.ndarray, n: int, b: int, ib: int, nthreads: int):
+    """Algorithm 1 / 2 / 3 with the oracle's kernels on a host thread pool (the paper's
+    progress-table runtime); bitwise equal to the sequential drivers.
+    Returns (aux or None, ipiv or None, info)."""
+    p = n // b
+    a = {"chol": 0, "qr": 1, "lu": 2}[alg]
+    aux = np.zeros(max(1, p * p * ib * b), dtype=np.float64)
+    piv = np.zeros(max(1, p * p * b), dtype=np.int32)
+    info = lib().o_factor_par(a, n, b, ib, _d(tiles), _d(aux), _i(piv), int(nthreads))
+    return (None if a == 0 else aux), (piv if a == 2 else None), info
 
 
 def lu_decisions(tiles: np.ndarray, n: int, b: int, ib: int):

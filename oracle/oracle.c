@@ -33,6 +33,7 @@
  * [1,2b] with bottom row r encoded as b+r+1.
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -864,4 +865,218 @@ double o_kernel_flops(int kind, double b, double s) {
     case 11: return 2.0 * b * b * b + s * b * b;       /* SSSSM */
     default: return NAN;
   }
+}
+
+
+/* ====================================================================================
+ * Host multicore baseline: the oracle's tile kernels under a thread-pool DAG executor —
+ * the paper's runtime (§4.1): a shared progress table (in-degree
+ * counters), every thread repeatedly takes the highest-priority ready task (kind ranks
+ * panel > couple-factor > row-update > couple-update; ties by program
+ * order) and releases its successors when done.  Dependencies come from each task's
+ * read / write sets over tiles, with diagonal tiles of QR / LU split into the V / L
+ * (strictly lower) and R / U (upper) regions (TSQRT / TSTRF touch only the upper one).
+ * Every tile's updates keep their program order, so the result is bitwise that of the
+ * sequential drivers.  Reported as a baseline only (bench.py cpu_baseline).
+ * ================================================================================== */
+typedef struct { int kind, k, i, j; } OTask;
+typedef struct {
+  int alg; int64_t n, b, ib, p;
+  double *A, *aux; int32_t* ipiv;
+  OTask* t; int nt;
+  int *indeg, *soff, *succ, *level;
+  int *heap; int nheap;            /* ready tasks, min (level, index) */
+  int done, abort_, info;
+  pthread_mutex_t mu; pthread_cond_t cv;
+} OPool;
+
+static int o_key_less(const OPool* P, int a, int b) {
+  return P->level[a] != P->level[b] ? P->level[a] < P->level[b] : a < b;
+}
+static void o_heap_push(OPool* P, int x) {
+  int c = P->nheap++;
+  P->heap[c] = x;
+  while (c > 0) {
+    int par = (c - 1) / 2;
+    if (!o_key_less(P, P->heap[c], P->heap[par])) break;
+    int t = P->heap[c]; P->heap[c] = P->heap[par]; P->heap[par] = t; c = par;
+  }
+}
+static int o_heap_pop(OPool* P) {
+  int top = P->heap[0];
+  P->heap[0] = P->heap[--P->nheap];
+  int c = 0;
+  for (;;) {
+    int l = 2 * c + 1, r = l + 1, m = c;
+    if (l < P->nheap && o_key_less(P, P->heap[l], P->heap[m])) m = l;
+    if (r < P->nheap && o_key_less(P, P->heap[r], P->heap[m])) m = r;
+    if (m == c) break;
+    int t = P->heap[c]; P->heap[c] = P->heap[m]; P->heap[m] = t; c = m;
+  }
+  return top;
+}
+
+static void o_run_task(OPool* P, const OTask* T) {
+  int64_t p = P->p, b = P->b, ib = P->ib;
+  double* A = P->A;
+  int k = T->k, i = T->i, j = T->j, info = 0;
+  switch (T->kind) {
+    case 0: info = o_potrf(b, OT(A, p, b, k, k)); if (info) info += (int)(k * b); break;
+    case 1: o_trsm(b, OT(A, p, b, k, k), OT(A, p, b, i, k)); break;
+    case 2: o_syrk(b, OT(A, p, b, i, k), OT(A, p, b, i, i)); break;
+    case 3: o_gemm_nt(b, OT(A, p, b, i, k), OT(A, p, b, j, k), OT(A, p, b, i, j)); break;
+    case 4: o_geqrt(b, ib, OT(A, p, b, k, k), OSTRIP(P->aux, p, b, ib, k, k)); break;
+    case 5: o_larfb(b, ib, OT(A, p, b, k, k), OSTRIP(P->aux, p, b, ib, k, k), OT(A, p, b, k, j)); break;
+    case 6: o_tsqrt(b, ib, OT(A, p, b, k, k), OT(A, p, b, i, k), OSTRIP(P->aux, p, b, ib, i, k)); break;
+    case 7: o_ssrfb(b, ib, OT(A, p, b, i, k), OSTRIP(P->aux, p, b, ib, i, k), OT(A, p, b, k, j), OT(A, p, b, i, j)); break;
+    case 8: o_getrf(b, ib, OT(A, p, b, k, k), OPIV(P->ipiv, p, b, k, k), &info); if (info) info += (int)(k * b); break;
+    case 9: o_gessm(b, ib, OT(A, p, b, k, k), OPIV(P->ipiv, p, b, k, k), OT(A, p, b, k, j)); break;
+    case 10:
+      o_tstrf(b, ib, OT(A, p, b, k, k), OT(A, p, b, i, k), OSTRIP(P->aux, p, b, ib, i, k), OPIV(P->ipiv, p, b, i, k), &info);
+      if (info) info += (int)(k * b);
+      break;
+    case 11:
+      o_ssssm(b, ib, OT(A, p, b, i, k), OSTRIP(P->aux, p, b, ib, i, k), OPIV(P->ipiv, p, b, i, k), OT(A, p, b, k, j),
+              OT(A, p, b, i, j));
+      break;
+  }
+  if (info) {
+    pthread_mutex_lock(&P->mu);
+    if (!P->info || info < P->info) P->info = info;
+    if (T->kind == 0) P->abort_ = 1;  /* Cholesky stops at the first failure (Z3) */
+    pthread_mutex_unlock(&P->mu);
+  }
+}
+
+static void* o_worker(void* arg) {
+  OPool* P = (OPool*)arg;
+  pthread_mutex_lock(&P->mu);
+  for (;;) {
+    while (P->nheap == 0 && P->done < P->nt && !P->abort_) pthread_cond_wait(&P->cv, &P->mu);
+    if (P->abort_ || P->done >= P->nt) break;
+    int t = o_heap_pop(P);
+    pthread_mutex_unlock(&P->mu);
+    o_run_task(P, &P->t[t]);
+    pthread_mutex_lock(&P->mu);
+    P->done++;
+    for (int e = P->soff[t]; e < P->soff[t + 1]; ++e)
+      if (--P->indeg[P->succ[e]] == 0) o_heap_push(P, P->succ[e]);
+    pthread_cond_broadcast(&P->cv);
+  }
+  pthread_cond_broadcast(&P->cv);
+  pthread_mutex_unlock(&P->mu);
+  return NULL;
+}
+
+/* alg 0 chol, 1 qr, 2 lu; aux = T / L strips, ipiv (LU).  Returns info. */
+int o_factor_par(int alg, int64_t n, int64_t b, int64_t ib, double* A, double* aux, int32_t* ipiv, int nthreads) {
+  int64_t p = n / b;
+  int64_t cap = alg == 0 ? p * (p + 1) * (p + 2) / 6 + p * p : p * (p + 1) * (2 * p + 1) / 6 + p * p;
+  OTask* t = (OTask*)malloc(sizeof(OTask) * cap);
+  int nt = 0;
+  if (alg == 0) {
+    for (int k = 0; k < p; ++k) {
+      t[nt++] = (OTask){0, k, k, k};
+      for (int i = k + 1; i < p; ++i) t[nt++] = (OTask){1, k, i, k};
+      for (int i = k + 1; i < p; ++i)
+        for (int j = k + 1; j <= i; ++j) t[nt++] = (OTask){i == j ? 2 : 3, k, i, j};
+    }
+  } else {
+    int F = alg == 1 ? 4 : 8;
+    for (int k = 0; k < p; ++k) {
+      t[nt++] = (OTask){F, k, k, k};
+      for (int j = k + 1; j < p; ++j) t[nt++] = (OTask){F + 1, k, k, j};
+      for (int i = k + 1; i < p; ++i) {
+        t[nt++] = (OTask){F + 2, k, i, k};
+        for (int j = k + 1; j < p; ++j) t[nt++] = (OTask){F + 3, k, i, j};
+      }
+    }
+  }
+  /* resources: tile (i,j) region r -> 2*(i + j*p) + r (r = 1: upper region of a diagonal
+   * tile in QR / LU); strip + pivots (i,k) -> 2*p*p + i + k*p */
+  int64_t nres = 3 * p * p;
+  int* lastw = (int*)malloc(sizeof(int) * nres);
+  int** rd = (int**)calloc(nres, sizeof(int*));
+  int* nrd = (int*)calloc(nres, sizeof(int));
+  int* crd = (int*)calloc(nres, sizeof(int));
+  for (int64_t x = 0; x < nres; ++x) lastw[x] = -1;
+  int* pcnt = (int*)calloc(nt, sizeof(int));
+  int pcap = 16 * nt + 16;
+  int* pl = (int*)malloc(sizeof(int) * pcap);  /* (task, pred) pairs */
+  int np = 0;
+  int* level = (int*)malloc(sizeof(int) * nt);
+#define TILE(a, c, r) (2 * ((int64_t)(a) + (int64_t)(c) * p) + (r))
+#define STRIP_(a, c) (2 * p * p + (int64_t)(a) + (int64_t)(c) * p)
+  for (int x = 0; x < nt; ++x) {
+    const OTask* T = &t[x];
+    int64_t rs[6], ws[6];
+    int nr = 0, nw = 0;
+    int k = T->k, i = T->i, j = T->j;
+    switch (T->kind) {
+      case 0: ws[nw++] = TILE(k, k, 0); break;
+      case 1: rs[nr++] = TILE(k, k, 0); ws[nw++] = TILE(i, k, 0); break;
+      case 2: rs[nr++] = TILE(i, k, 0); ws[nw++] = TILE(i, i, 0); break;
+      case 3: rs[nr++] = TILE(i, k, 0); rs[nr++] = TILE(j, k, 0); ws[nw++] = TILE(i, j, 0); break;
+      case 4: case 8: ws[nw++] = TILE(k, k, 0); ws[nw++] = TILE(k, k, 1); ws[nw++] = STRIP_(k, k); break;
+      case 5: case 9: rs[nr++] = TILE(k, k, 0); rs[nr++] = STRIP_(k, k); ws[nw++] = TILE(k, j, 0); break;
+      case 6: case 10: ws[nw++] = TILE(k, k, 1); ws[nw++] = TILE(i, k, 0); ws[nw++] = STRIP_(i, k); break;
+      default:  /* 7, 11: reads (i,k) + strip, writes (k,j) and (i,j) (both regions if diagonal) */
+        rs[nr++] = TILE(i, k, 0); rs[nr++] = STRIP_(i, k);
+        ws[nw++] = TILE(k, j, 0);
+        ws[nw++] = TILE(i, j, 0);
+        if (i == j) ws[nw++] = TILE(i, j, 1);
+        break;
+    }
+    switch (T->kind) {
+      case 0: case 4: case 8: level[x] = 0; break;
+      case 1: case 6: case 10: level[x] = 1; break;
+      case 5: case 9: level[x] = 2; break;
+      default: level[x] = 3;
+    }
+#define ADDP(q) do { if ((q) >= 0 && (q) != x) { if (np == pcap) { pcap *= 2; pl = (int*)realloc(pl, sizeof(int) * pcap); } pl[np++] = (q); pcnt[x]++; } } while (0)
+    for (int a = 0; a < nr; ++a) {
+      ADDP(lastw[rs[a]]);
+      if (nrd[rs[a]] == crd[rs[a]]) { crd[rs[a]] = crd[rs[a]] ? 2 * crd[rs[a]] : 4; rd[rs[a]] = (int*)realloc(rd[rs[a]], sizeof(int) * crd[rs[a]]); }
+      rd[rs[a]][nrd[rs[a]]++] = x;
+    }
+    for (int a = 0; a < nw; ++a) {
+      ADDP(lastw[ws[a]]);
+      for (int r = 0; r < nrd[ws[a]]; ++r) ADDP(rd[ws[a]][r]);
+      nrd[ws[a]] = 0;
+      lastw[ws[a]] = x;
+    }
+#undef ADDP
+  }
+#undef TILE
+#undef STRIP_
+  /* pl holds preds grouped by task in order; build successor CSR (duplicates harmless:
+   * each duplicate edge is counted once in indeg and once in succ) */
+  int* indeg = (int*)calloc(nt, sizeof(int));
+  int* soff = (int*)calloc(nt + 1, sizeof(int));
+  { int q = 0; for (int x = 0; x < nt; ++x) for (int c = 0; c < pcnt[x]; ++c, ++q) { soff[pl[q] + 1]++; indeg[x]++; } }
+  for (int x = 0; x < nt; ++x) soff[x + 1] += soff[x];
+  int* succ = (int*)malloc(sizeof(int) * (np + 1));
+  int* fill = (int*)malloc(sizeof(int) * (nt + 1));
+  memcpy(fill, soff, sizeof(int) * (nt + 1));
+  { int q = 0; for (int x = 0; x < nt; ++x) for (int c = 0; c < pcnt[x]; ++c, ++q) succ[fill[pl[q]]++] = x; }
+  OPool P;
+  memset(&P, 0, sizeof(P));
+  P.alg = alg; P.n = n; P.b = b; P.ib = ib; P.p = p; P.A = A; P.aux = aux; P.ipiv = ipiv;
+  P.t = t; P.nt = nt; P.indeg = indeg; P.soff = soff; P.succ = succ; P.level = level;
+  P.heap = (int*)malloc(sizeof(int) * (nt + 1));
+  pthread_mutex_init(&P.mu, NULL);
+  pthread_cond_init(&P.cv, NULL);
+  for (int x = 0; x < nt; ++x)
+    if (indeg[x] == 0) o_heap_push(&P, x);
+  if (nthreads < 1) nthreads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * nthreads);
+  for (int w = 0; w < nthreads; ++w) pthread_create(&th[w], NULL, o_worker, &P);
+  for (int w = 0; w < nthreads; ++w) pthread_join(th[w], NULL);
+  int info = P.info;
+  pthread_mutex_destroy(&P.mu);
+  pthread_cond_destroy(&P.cv);
+  for (int64_t x = 0; x < nres; ++x) free(rd[x]);
+  free(rd); free(nrd); free(crd); free(lastw); free(pcnt); free(pl); free(level); free(indeg); free(soff);
+  free(succ); free(fill); free(P.heap); free(th); free(t);
+  return info;
 }

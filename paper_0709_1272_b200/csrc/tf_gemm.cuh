@@ -98,7 +98,10 @@ struct GemmLayout {
   static constexpr int TOTAL = NST * STAGE;                        // doubles
 };
 
-template <int BM, int BN, int WM, int WN, bool AK, bool BK>
+// NEG: the A fragments enter the product negated (the sign folds into the DMMA operand
+// modifier), so acc += -Aop*Bop: with acc preloaded from C (load_acc) the update C -= A B
+// ends with plain stores (store_acc) instead of a dependent read-modify-write epilogue.
+template <int BM, int BN, int WM, int WN, bool AK, bool BK, bool NEG = false>
 struct Gemm {
   static_assert(WM * WN == TF_WARPS, "all warps own a sub-tile");
   static constexpr int TM = BM / WM, TN = BN / WN;  // warp tile
@@ -197,8 +200,8 @@ struct Gemm {
 #pragma unroll
         for (int i = 0; i < MI; ++i) {
           const double2 v = *reinterpret_cast<const double2*>(sA + (wm * TM + 8 * i + r) * Lay::SK + 8 * s + 2 * q);
-          a[0][i] = v.x;
-          a[1][i] = v.y;
+          a[0][i] = NEG ? -v.x : v.x;
+          a[1][i] = NEG ? -v.y : v.y;
         }
       }
       if (BK) {
@@ -217,8 +220,8 @@ struct Gemm {
 #pragma unroll
           for (int i2 = 0; i2 < MI / 2; ++i2) {
             const double2 v = *reinterpret_cast<const double2*>(sA + kr * Lay::SMN_A + wm * TM + 16 * i2 + 2 * r);
-            a[h][2 * i2] = v.x;
-            a[h][2 * i2 + 1] = v.y;
+            a[h][2 * i2] = NEG ? -v.x : v.x;
+            a[h][2 * i2 + 1] = NEG ? -v.y : v.y;
           }
         }
         if (!BK) {
@@ -241,10 +244,17 @@ struct Gemm {
         } else
 #endif
         {
+#ifdef TF_JI
+#pragma unroll
+          for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int i = 0; i < MI; ++i) dmma(acc[i][j], a[h][i], b[h][j]);
+#else
 #pragma unroll
           for (int i = 0; i < MI; ++i)
 #pragma unroll
             for (int j = 0; j < NI; ++j) dmma(acc[i][j], a[h][i], b[h][j]);
+#endif
         }
       }
     }
@@ -514,6 +524,67 @@ struct Gemm {
             }
           }
       }
+    }
+  }
+
+  // acc <- C (M x N block, ld ldc), the labels of sub_from; out-of-range elements 0.
+  // Requires !AK (m-contiguous A: fragment rows pair up along a column of C).
+  __device__ __forceinline__ void load_acc(const double* C, int ldc, int M, int N) {
+    static_assert(!AK, "load_acc: m-contiguous A only");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const int r = lane >> 2, q = lane & 3;
+    const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc & 1) == 0);
+#pragma unroll
+    for (int i2 = 0; i2 < MI / 2; ++i2) {
+      const int rr = wm * TM + 16 * i2 + 2 * r;
+#pragma unroll
+      for (int j = 0; j < NI; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cl = 2 * q + e;
+          const int cc = BK ? (wn * TN + 8 * j + cl) : (wn * TN + 16 * (j >> 1) + 2 * cl + (j & 1));
+          const double* p = C + rr + (size_t)cc * ldc;
+          double2 v = make_double2(0.0, 0.0);
+          if (cc < N) {
+            if (vec && rr + 1 < M) v = __ldcg(reinterpret_cast<const double2*>(p));
+            else {
+              if (rr < M) v.x = __ldcg(p);
+              if (rr + 1 < M) v.y = __ldcg(p + 1);
+            }
+          }
+          acc[2 * i2][j][e] = v.x;
+          acc[2 * i2 + 1][j][e] = v.y;
+        }
+    }
+  }
+  // C <- acc (the labels of sub_from; optional lower mask as sub_from).
+  __device__ __forceinline__ void store_acc(double* C, int ldc, int M, int N, bool mask, int row0, int col0) const {
+    static_assert(!AK, "store_acc: m-contiguous A only");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const int r = lane >> 2, q = lane & 3;
+    const bool vec = ((reinterpret_cast<uintptr_t>(C) & 15) == 0) && ((ldc & 1) == 0);
+#pragma unroll
+    for (int i2 = 0; i2 < MI / 2; ++i2) {
+      const int rr = wm * TM + 16 * i2 + 2 * r;
+#pragma unroll
+      for (int j = 0; j < NI; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cl = 2 * q + e;
+          const int cc = BK ? (wn * TN + 8 * j + cl) : (wn * TN + 16 * (j >> 1) + 2 * cl + (j & 1));
+          if (cc >= N) continue;
+          double* p = C + rr + (size_t)cc * ldc;
+          const bool w0 = rr < M && !(mask && row0 + rr < col0 + cc);
+          const bool w1 = rr + 1 < M && !(mask && row0 + rr + 1 < col0 + cc);
+          if (w0 && w1 && vec) {
+            *reinterpret_cast<double2*>(p) = make_double2(acc[2 * i2][j][e], acc[2 * i2 + 1][j][e]);
+          } else {
+            if (w0) p[0] = acc[2 * i2][j][e];
+            if (w1) p[1] = acc[2 * i2 + 1][j][e];
+          }
+        }
     }
   }
 

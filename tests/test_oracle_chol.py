@@ -114,3 +114,32 @@ def test_pack_spec_example():
     # tile (i=1, j=0) 0-based is at offset (1 + 0*2)*4
     assert list(F[4:8]) == [31.0, 41.0, 32.0, 42.0]
     assert np.array_equal(oracle.unpack(F, 4, 4, 2), D)
+
+
+def test_host_pool_bitwise_equals_sequential():
+    """The multicore baseline (oracle kernels on a host thread pool driven by the DAG,
+    the paper's progress-table runtime) reproduces the sequential
+    drivers bitwise for all three algorithms (SPEC.md:369 schedule independence)."""
+    import oracle as o
+    for alg, gen in (("chol", tilegen.spd), ("qr", tilegen.uniform), ("lu", tilegen.normal)):
+        n, b, ib = 160, 32, 8
+        A = gen(n, 9)
+        F1, F2 = o.pack(A, b), o.pack(A, b)
+        if alg == "chol":
+            i1 = o.chol(F1, n, b)
+            _, _, i2 = o.factor_par(alg, F2, n, b, ib, 6)
+            assert i1 == i2 == 0
+        elif alg == "qr":
+            T1 = o.qr(F1, n, b, ib)
+            T2, _, _ = o.factor_par(alg, F2, n, b, ib, 6)
+            assert np.array_equal(T1, T2)
+        else:
+            L1, p1, i1 = o.lu(F1, n, b, ib)
+            L2, p2, i2 = o.factor_par(alg, F2, n, b, ib, 6)
+            assert np.array_equal(L1, L2) and np.array_equal(p1, p2) and i1 == i2
+        assert np.array_equal(F1, F2), alg
+    # Cholesky failure: same info as the sequential driver
+    A = tilegen.spd(128, 1)
+    A[70, 70] = -1e6
+    F = o.pack(A, 32)
+    assert o.factor_par("chol", F, 128, 32, 8, 4)[2] == o.chol(o.pack(A, 32), 128, 32)

@@ -241,8 +241,18 @@ def run_e2e(tf, torch, cfg, steps, seed=0):
         torch.cuda.synchronize()
         if s > 0:  # first call allocates the library's device buffers
             ms.append(e0.elapsed_time(e1))
-    h2d = n * n * 8
-    d2h = n * n * 8 + (hAux.numel() * 8 if hAux is not None else 0) + (hPiv.numel() * 4 if hPiv is not None else 0) + 4
+    # bytes the call moves (tile_factor_host streams tile columns: Cholesky only the lower
+    # tiles it reads / writes; QR / LU all tiles plus the T / L strips and pivot vectors
+    # (i, k), i >= k, that the factorization writes); serial mode (TF_E2E_SERIAL) moves
+    # the whole buffers
+    p = n // b
+    serial = bool(int(os.environ.get("TF_E2E_SERIAL", "0") or 0))
+    tiles = p * p if (cfg["kind"] != "chol" or serial) else p * (p + 1) // 2
+    strips = p * p if serial else (p * (p + 1) // 2 if cfg["kind"] == "qr" else p * (p - 1) // 2)
+    pivs = p * p if serial else p * (p + 1) // 2
+    h2d = tiles * b * b * 8
+    d2h = tiles * b * b * 8 + (strips * ib * b * 8 if hAux is not None else 0) + \
+        (pivs * b * 4 if hPiv is not None else 0) + (4 if cfg["kind"] != "qr" else 0)
     del hA, host0, hAux, hPiv
     return ms, h2d, d2h, int(hInfo.item())
 
@@ -498,7 +508,9 @@ def run_ours(args, rank, world, local_rank):
         em = sum(ems) / len(ems)
         e2e = {"value": round(lapack_flops(cfg["kind"], n) / (em * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
                "ms_per_step": round(em, 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "api": "tile_factor_host (pinned host BDL buffer)"}
+               "api": "tile_factor_host (pinned host BDL buffer; tile columns streamed in / out on two copy "
+                      "streams, overlapped with the factorization)"
+                      if not os.environ.get("TF_E2E_SERIAL") else "tile_factor_host (serial copies)"}
     elif world > 1 and res.get("e2e"):
         t = torch.tensor([res["e2e"]["ms"]], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

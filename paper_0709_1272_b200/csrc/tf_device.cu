@@ -88,6 +88,34 @@ __device__ inline void sched_push(const Sched& S, int s) {
   for (int x = 0; x < d.nitems; ++x) q[x] = d.item0 + x;
 }
 
+// Completion of task t by a single thread (the scheduler's ARRIVE tasks): successors'
+// counters decremented, ready ones pushed, the task counted.
+__device__ inline void complete_task_single(const Sched& S, int t) {
+  fence_ar_gpu();
+  for (int e = S.succ_off[t]; e < S.succ_off[t + 1]; ++e) {
+    const int s = S.succ[e];
+    if (atomicSub(&S.indeg[s], 1) == 1) {
+      fence_ar_gpu();
+      sched_push(S, s);
+    }
+  }
+  fence_ar_gpu();
+  atomicAdd(S.ndone, 1);
+}
+
+// Copy overlap: if the next pending tile column has arrived (its flag was written by the
+// H2D copy stream after the column's data), complete its ARRIVE task.  One poller wins the
+// column by CAS.  Returns true if a column was released.
+__device__ inline bool poll_arrivals(const Sched& S) {
+  if (S.narrive == 0) return false;
+  const int j = ld_volatile(S.arrive_next);
+  if (j >= S.narrive || ld_acquire_sys(S.arrive_flags + j) == 0) return false;
+  if (atomicCAS(S.arrive_next, j, j + 1) != j) return false;
+  fence_ar_sys();  // the column's bytes (copy engine) before the tasks that read them
+  complete_task_single(S, S.arrive_task0 + j);
+  return true;
+}
+
 // Pop the next item: highest non-empty level first, FIFO inside a level.
 // Returns item id, -1 when every task has completed, -2 on abort.
 __device__ inline int sched_pop(const Sched& S, const Dist& D, int* info) {
@@ -124,6 +152,7 @@ __device__ inline int sched_pop(const Sched& S, const Dist& D, int* info) {
     }
     if (!retry) {
       if (ld_volatile(S.ndone) >= S.ntasks) return -1;
+      if (poll_arrivals(S)) { idle0 = 0; continue; }
       if (D.timeout_ns > 0) {
         const long long now = globaltimer();
         if (idle0 == 0) idle0 = now;
@@ -326,6 +355,12 @@ __device__ inline void run_item(const Prob& P, const Sched& S, const Dist& D, co
     case K_XGEMM: v_xgemm(cx, a.T(i, k), a.X(k, j), a.X(i, j), sub); break;
     case K_XUNSSSSM: v_unssssm(cx, a.T(i, k), a.STRIP(i, k), a.PIV(i, k), a.X(k, j), a.X(i, j), sub); break;
     case K_XUNGESSM: v_ungessm(cx, a.T(k, k), a.PIV(k, k), a.X(k, j), sub); break;
+    case K_DONE:  // every tile of column d.j is final: release the D2H copy of that column
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        st_release_sys(S.done_flags + d.j, 1);
+      }
+      break;
     case K_SEND: send_item(a, d, sub); break;
     case K_RECV: break;  // the data is already in the cache; completing releases the consumers
     default: break;

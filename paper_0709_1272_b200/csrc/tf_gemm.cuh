@@ -455,7 +455,8 @@ struct Gemm {
   }
 
   // C -= acc (see sub_store).
-  __device__ __forceinline__ void sub_from(double* C, int ldc, int M, int N, bool mask, int row0, int col0) const {
+  __device__ __forceinline__ void sub_from(double* C, int ldc, int M, int N, bool mask, int row0, int col0,
+                                           bool red = false) const {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = warp / WN, wn = warp % WN;
     const int r = lane >> 2, q = lane & 3;
@@ -480,6 +481,27 @@ struct Gemm {
             const int cl = 2 * q + e;
             const int cc = BK ? (wn * TN + 8 * j + cl) : (wn * TN + 16 * (j >> 1) + 2 * cl + (j & 1));
             if (rr < M && cc < N && !(mask && row0 + rr < col0 + cc)) C[rr + (size_t)cc * ldc] = cv[j][e] - acc[i][j][e];
+          }
+      }
+      return;
+    }
+    if (red && !AK) {
+      // fire-and-forget L2 reductions: C += -acc, one IEEE add per element as C - acc (the
+      // tile has a single writer at a time, so the result is the RMW's bitwise); no load
+      // round trips in the epilogue
+#pragma unroll
+      for (int i2 = 0; i2 < MI / 2; ++i2) {
+        const int rr = wm * TM + 16 * i2 + 2 * r;
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cl = 2 * q + e;
+            const int cc = BK ? (wn * TN + 8 * j + cl) : (wn * TN + 16 * (j >> 1) + 2 * cl + (j & 1));
+            if (cc >= N) continue;
+            double* p = C + rr + (size_t)cc * ldc;
+            if (rr < M && !(mask && row0 + rr < col0 + cc)) red_add_f64(p, -acc[2 * i2][j][e]);
+            if (rr + 1 < M && !(mask && row0 + rr + 1 < col0 + cc)) red_add_f64(p + 1, -acc[2 * i2 + 1][j][e]);
           }
       }
       return;
@@ -611,10 +633,12 @@ struct Gemm {
 // For m-contiguous A the two rows of a fragment pair are adjacent in a column of C, so
 // the read-modify-write uses 128-bit accesses, with all loads of a row pair issued
 // before any store (one L2 round trip per pair instead of one per element).
+// red: subtract with L2 reductions (red.global.add.f64) instead of load + store — for task
+// epilogues whose C is not read back by the same CTA within the item (GEMM / SYRK).
 template <class G>
 __device__ __forceinline__ void sub_store(const G& g, double* C, int ldc, int M, int N, bool lower_mask = false,
-                                          int row0 = 0, int col0 = 0) {
-  g.sub_from(C, ldc, M, N, lower_mask, row0, col0);
+                                          int row0 = 0, int col0 = 0, bool red = false) {
+  g.sub_from(C, ldc, M, N, lower_mask, row0, col0, red);
 }
 
 // Warm L2 with the M x N block of C (column-major, ld ldc) ahead of its epilogue.

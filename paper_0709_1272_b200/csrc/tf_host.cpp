@@ -250,14 +250,64 @@ void finalize_dag(HostDag& G, const std::vector<std::vector<int>>& preds) {
   for (int l = 0; l < NLEV; ++l) G.qbase[l + 1] = G.qbase[l] + lev_items[l];
   G.roots.clear();
   for (int t = 0; t < nt; ++t)
-    if (G.indeg0[t] == 0 && G.tasks[t].kind != K_RECV) G.roots.push_back(t);
+    if (G.indeg0[t] == 0 && G.tasks[t].kind != K_RECV && G.tasks[t].kind != K_ARRIVE) G.roots.push_back(t);
 }
 
-void build_dag(HostDag& G, int alg, int p, int b, int ib, int policy, int q = 0, int qc = -1) {
+// Host <-> device copy overlap (tile_factor_host): ARRIVE(j) before the first task that
+// touches a tile of column j, DONE(j) after the last task that writes one.  Tile sets per
+// task as in the a13 rules (reads of the panel tiles, writes of the outputs).
+void add_copy_tasks(int alg, int p, int b, int ib, std::vector<TaskD>& tasks, std::vector<std::vector<int>>& preds) {
+  const int nt = (int)tasks.size();
+  std::vector<char> touched((size_t)p * p, 0);
+  std::vector<int> lastw((size_t)p * p, -1);
+  auto id = [&](int i, int j) { return (size_t)i + (size_t)j * p; };
+  const int a0 = nt;  // ARRIVE(j) = a0 + j, DONE(j) = a0 + p + j
+  for (int j = 0; j < p; ++j) tasks.push_back(TaskD{K_ARRIVE, j, j, j, 1, 0, 0, 0});
+  for (int j = 0; j < p; ++j) tasks.push_back(TaskD{K_DONE, j, j, j, 1, 0, 0, 0});
+  preds.resize(tasks.size());
+  for (int t = 0; t < nt; ++t) {
+    const TaskD& d = tasks[t];
+    const int k = d.k, i = d.i, j = d.j;
+    int rd[3][2], wr[2][2], nr = 0, nw = 0;
+    auto R = [&](int r, int c) { rd[nr][0] = r; rd[nr][1] = c; ++nr; };
+    auto W = [&](int r, int c) { wr[nw][0] = r; wr[nw][1] = c; ++nw; };
+    if (alg == 0) {
+      switch (d.kind) {
+        case 0: W(k, k); break;
+        case 1: R(k, k); W(i, k); break;
+        case 2: R(i, k); W(i, i); break;
+        default: R(i, k); R(j, k); W(i, j); break;
+      }
+    } else {
+      const int F = alg == 1 ? 4 : 8;
+      if (d.kind == F) W(k, k);
+      else if (d.kind == F + 1) { R(k, k); W(k, j); }
+      else if (d.kind == F + 2) { W(k, k); W(i, k); }
+      else { R(i, k); W(k, j); W(i, j); }
+    }
+    for (int x = 0; x < nr + nw; ++x) {
+      const int r = x < nr ? rd[x][0] : wr[x - nr][0], c = x < nr ? rd[x][1] : wr[x - nr][1];
+      if (!touched[id(r, c)]) {
+        touched[id(r, c)] = 1;
+        if (std::find(preds[t].begin(), preds[t].end(), a0 + c) == preds[t].end()) preds[t].push_back(a0 + c);
+      }
+    }
+    for (int x = 0; x < nw; ++x) lastw[id(wr[x][0], wr[x][1])] = t;
+  }
+  for (int j = 0; j < p; ++j)
+    for (int i = 0; i < p; ++i) {
+      const int w = lastw[id(i, j)];
+      auto& pr = preds[a0 + p + j];
+      if (w >= 0 && std::find(pr.begin(), pr.end(), w) == pr.end()) pr.push_back(w);
+    }
+}
+
+void build_dag(HostDag& G, int alg, int p, int b, int ib, int policy, int q = 0, int qc = -1, int e2e = 0) {
   G.alg = alg; G.p = p; G.b = b; G.policy = policy;
   std::vector<std::vector<int>> preds;
   if (alg >= ALG_GETRS) solve_tasks(alg, p, b, ib, q, policy, G.tasks, preds);
   else global_tasks(alg, p, b, ib, policy, G.tasks, preds, qc);
+  if (e2e) add_copy_tasks(alg, p, b, ib, G.tasks, preds);
   finalize_dag(G, preds);
 }
 
@@ -386,7 +436,7 @@ struct DevDag {
   SendEnt* sends = nullptr;
 };
 
-std::map<std::tuple<int, int, int, int, int, int, int, int>, DevDag> g_dags;  // (dev, alg, p, b, ib, policy, q, qc)
+std::map<std::tuple<int, int, int, int, int, int, int, int, int>, DevDag> g_dags;  // (dev, alg, p, b, ib, policy, q, qc, e2e)
 
 template <class T>
 int upload(T** dst, const std::vector<T>& v) {
@@ -417,13 +467,13 @@ void free_dag(DevDag& D) {
   D = DevDag();
 }
 
-int get_dag(int dev, int alg, int p, int b, int ib, DevDag** out, int q = 0, int qc = -1) {
-  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy, q, qc);
+int get_dag(int dev, int alg, int p, int b, int ib, DevDag** out, int q = 0, int qc = -1, int e2e = 0) {
+  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy, q, qc, e2e);
   auto it = g_dags.find(key);
   if (it != g_dags.end()) { *out = &it->second; return 0; }
   DevDag D;
   D.h = std::make_shared<HostDag>();
-  build_dag(*D.h, alg, p, b, ib, g_policy, q, qc);
+  build_dag(*D.h, alg, p, b, ib, g_policy, q, qc, e2e);
   int rc;
   if ((rc = upload_dag(D))) return rc;
   auto res = g_dags.emplace(key, D);
@@ -456,9 +506,11 @@ void release(Buf& b) {
 
 struct Workspace {
   Buf state, q, vx, scratch, info, trace, xt;
-  Buf hostA, hostAux, hostPiv;  // device buffers for tile_factor_host
+  Buf hostA, hostAux, hostPiv, flags;  // device buffers for tile_factor_host
   int64_t last_items = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t cin = nullptr, cout = nullptr;  // tile_factor_host copy streams
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
 
@@ -523,9 +575,11 @@ long long watchdog_ns() {
 }
 
 // m_rows >= 0: QR / LU of an m_rows x n matrix (p = m_rows/b tile rows, n/b tile columns).
+// copy_flags (tile_factor_host): [p] arrive flags, [p] done flags, [1] arrive cursor; the
+// DAG then has ARRIVE / DONE tasks (add_copy_tasks).
 int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, double* aux, int32_t* ipiv,
                       int32_t* d_info, cudaStream_t stream, double* X = nullptr, int q = 0, int nopiv = 0,
-                      int64_t m_rows = -1) {
+                      int64_t m_rows = -1, int* copy_flags = nullptr) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   int dev;
   TF_CUDA(cudaGetDevice(&dev));
@@ -534,7 +588,7 @@ int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, dou
   const int p = (int)((m_rows >= 0 ? m_rows : n) / b);
   const int qc = m_rows >= 0 ? (int)(n / b) : -1;
   DevDag* D;
-  if ((rc = get_dag(dev, alg, p, (int)b, (int)ib, &D, q, qc))) return rc;
+  if ((rc = get_dag(dev, alg, p, (int)b, (int)ib, &D, q, qc, copy_flags ? 1 : 0))) return rc;
   const HostDag& H = *D->h;
   Workspace& W = g_ws[std::make_pair(dev, stream)];
   W.stream = stream;
@@ -571,6 +625,13 @@ int run_factorization(int alg, int64_t n, int64_t b, int64_t ib, double* dA, dou
   P.X = X;
   P.q = q;
   P.nopiv = nopiv;
+  if (copy_flags) {
+    S.arrive_flags = copy_flags;
+    S.done_flags = copy_flags + p;
+    S.arrive_next = copy_flags + 2 * p;
+    S.arrive_task0 = (int)H.tasks.size() - 2 * p;
+    S.narrive = p;
+  }
   R.r[0].D.timeout_ns = watchdog_ns();
   TF_LAUNCH(launch_sched_reset(S, D->indeg0, H.nitems, P.info, stream));
   TF_LAUNCH(launch_sched_seed(S, D->roots, (int)H.roots.size(), stream));
@@ -931,6 +992,32 @@ int tile_unpack(int64_t m, int64_t n, int64_t b, const double* dTiles, double* d
   return 0;
 }
 
+// Stream memory operations (driver API, through the runtime's entry-point query so the
+// library keeps no link dependency on libcuda): the H2D copy stream writes a column's
+// arrival flag after its bytes; the D2H copy stream waits on a column's done flag.
+typedef int (*pfn_stream_value32)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+static pfn_stream_value32 g_write32 = nullptr, g_wait32 = nullptr;
+static int stream_memops() {
+  if (g_write32 && g_wait32) return 0;
+  cudaDriverEntryPointQueryResult q1, q2;
+  void *w = nullptr, *t = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &q1) != cudaSuccess ||
+      cudaGetDriverEntryPoint("cuStreamWaitValue32", &t, cudaEnableDefault, &q2) != cudaSuccess ||
+      q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !w || !t) {
+    cudaGetLastError();
+    set_err("stream memory operations unavailable");
+    return TF_ERR_UNSUPPORTED;
+  }
+  g_write32 = (pfn_stream_value32)w;
+  g_wait32 = (pfn_stream_value32)t;
+  return 0;
+}
+
+// End-to-end host-buffer path with the copies overlapped with the factorization: tile
+// column j goes host -> device on one copy stream (then its arrival flag), the DAG's first
+// task touching column j waits for that flag (ARRIVE(j)), and as soon as every tile of
+// column j is final (DONE(j)) a second copy stream brings it back while the trailing
+// updates run.  TF_E2E_SERIAL=1 selects the serial copy / factor / copy path.
 int tile_factor_host(int kind, int64_t n, int64_t b, int64_t ib, double* hA, double* hAux, int32_t* hIpiv,
                      int32_t* hInfo, tf_stream_t stream) {
   int rc = check_args(n, b, ib, hA);
@@ -947,23 +1034,87 @@ int tile_factor_host(int kind, int64_t n, int64_t b, int64_t ib, double* hA, dou
   const size_t an = (size_t)n * n;
   const size_t xn = kind == 0 ? 0 : tile_qr_t_elems(n, b, ib);
   const size_t pn = kind == 2 ? tile_lu_ipiv_elems(n, b) : 0;
+  const int64_t p = n / b;
   if ((rc = ensure(W->hostA, an * sizeof(double) + 64))) return rc;
   if (xn && (rc = ensure(W->hostAux, xn * sizeof(double)))) return rc;
   if (pn && (rc = ensure(W->hostPiv, pn * sizeof(int32_t) + 64))) return rc;
   double* dA = (double*)W->hostA.p;
+  double* dAux = (double*)W->hostAux.p;
+  int32_t* dPiv = (int32_t*)W->hostPiv.p;
   int32_t* dInfo = (int32_t*)((char*)W->hostA.p + an * sizeof(double));
-  TF_CUDA(cudaMemcpyAsync(dA, hA, an * sizeof(double), cudaMemcpyHostToDevice, s));
-  if (kind == 0) rc = tile_chol(n, b, ib, dA, dInfo, stream);
-  else if (kind == 1) rc = tile_qr(n, b, ib, dA, (double*)W->hostAux.p, stream);
-  else rc = tile_lu(n, b, ib, dA, (double*)W->hostAux.p, (int32_t*)W->hostPiv.p, dInfo, stream);
-  if (rc) return rc;
-  TF_CUDA(cudaMemcpyAsync(hA, dA, an * sizeof(double), cudaMemcpyDeviceToHost, s));
-  if (hAux && xn) TF_CUDA(cudaMemcpyAsync(hAux, W->hostAux.p, xn * sizeof(double), cudaMemcpyDeviceToHost, s));
-  if (hIpiv && pn) TF_CUDA(cudaMemcpyAsync(hIpiv, W->hostPiv.p, pn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  const char* ser = getenv("TF_E2E_SERIAL");
+  if ((ser && atoi(ser)) || stream_memops() != 0) {
+    TF_CUDA(cudaMemcpyAsync(dA, hA, an * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (kind == 0) rc = tile_chol(n, b, ib, dA, dInfo, stream);
+    else if (kind == 1) rc = tile_qr(n, b, ib, dA, dAux, stream);
+    else rc = tile_lu(n, b, ib, dA, dAux, dPiv, dInfo, stream);
+    if (rc) return rc;
+    TF_CUDA(cudaMemcpyAsync(hA, dA, an * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (hAux && xn) TF_CUDA(cudaMemcpyAsync(hAux, dAux, xn * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (hIpiv && pn) TF_CUDA(cudaMemcpyAsync(hIpiv, dPiv, pn * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    if (hInfo) {
+      if (kind == 1) *hInfo = 0;
+      else TF_CUDA(cudaMemcpyAsync(hInfo, dInfo, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    }
+    TF_CUDA(cudaStreamSynchronize(s));
+    return 0;
+  }
+  if (!W->cin) {
+    TF_CUDA(cudaStreamCreateWithFlags(&W->cin, cudaStreamNonBlocking));
+    TF_CUDA(cudaStreamCreateWithFlags(&W->cout, cudaStreamNonBlocking));
+    TF_CUDA(cudaEventCreateWithFlags(&W->ev0, cudaEventDisableTiming));
+    TF_CUDA(cudaEventCreateWithFlags(&W->ev1, cudaEventDisableTiming));
+  }
+  if ((rc = ensure(W->flags, (size_t)(2 * p + 4) * sizeof(int)))) return rc;
+  int* flags = (int*)W->flags.p;
+  // flags reset on the compute stream, before either copy stream touches them
+  TF_CUDA(cudaMemsetAsync(flags, 0, (size_t)(2 * p + 4) * sizeof(int), s));
+  TF_CUDA(cudaEventRecord(W->ev0, s));
+  TF_CUDA(cudaStreamWaitEvent(W->cin, W->ev0, 0));
+  TF_CUDA(cudaStreamWaitEvent(W->cout, W->ev0, 0));
+  const size_t bb = (size_t)b * b, colA = (size_t)p * bb;
+  // Cholesky reads and writes only the lower tiles (i >= j) of column j
+  auto col_off = [&](int64_t j) { return kind == 0 ? (size_t)j * colA + (size_t)j * bb : (size_t)j * colA; };
+  auto col_len = [&](int64_t j) { return kind == 0 ? (size_t)(p - j) * bb : colA; };
+  for (int64_t j = 0; j < p; ++j) {
+    TF_CUDA(cudaMemcpyAsync(dA + col_off(j), hA + col_off(j), col_len(j) * sizeof(double), cudaMemcpyHostToDevice,
+                            W->cin));
+    if (g_write32(W->cin, (unsigned long long)(uintptr_t)(flags + j), 1u, 0u) != 0) {
+      set_err("cuStreamWriteValue32 failed");
+      return TF_ERR_CUDA;
+    }
+  }
+  if ((rc = run_factorization(kind, n, b, ib, dA, kind ? dAux : nullptr, kind == 2 ? dPiv : nullptr,
+                              kind == 1 ? nullptr : dInfo, s, nullptr, 0, 0, -1, flags)))
+    return rc;
+  for (int64_t j = 0; j < p; ++j) {
+    if (g_wait32(W->cout, (unsigned long long)(uintptr_t)(flags + p + j), 1u, 0u /* GEQ */) != 0) {
+      set_err("cuStreamWaitValue32 failed");
+      return TF_ERR_CUDA;
+    }
+    TF_CUDA(cudaMemcpyAsync(hA + col_off(j), dA + col_off(j), col_len(j) * sizeof(double), cudaMemcpyDeviceToHost,
+                            W->cout));
+    // T strips (i, j), i >= j; L strips (i, j), i > j; pivot vectors (i, j), i >= j (the
+    // ones the factorization writes)
+    const int64_t x0 = kind == 2 ? j + 1 : j;
+    const size_t sx = (size_t)(x0 + j * p) * ib * b, nx = (size_t)(p - x0) * ib * b;
+    const size_t sp = (size_t)(j + j * p) * b, npv = (size_t)(p - j) * b;
+    if (hAux && xn && nx)
+      TF_CUDA(cudaMemcpyAsync(hAux + sx, dAux + sx, nx * sizeof(double), cudaMemcpyDeviceToHost, W->cout));
+    if (hIpiv && pn)
+      TF_CUDA(cudaMemcpyAsync(hIpiv + sp, dPiv + sp, npv * sizeof(int32_t), cudaMemcpyDeviceToHost, W->cout));
+  }
+  TF_CUDA(cudaEventRecord(W->ev1, s));  // the factorization (and its info) finished
+  TF_CUDA(cudaStreamWaitEvent(W->cout, W->ev1, 0));
   if (hInfo) {
     if (kind == 1) *hInfo = 0;
-    else TF_CUDA(cudaMemcpyAsync(hInfo, dInfo, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    else TF_CUDA(cudaMemcpyAsync(hInfo, dInfo, sizeof(int32_t), cudaMemcpyDeviceToHost, W->cout));
   }
+  // the caller's stream orders after both copy streams (its events time the whole path)
+  TF_CUDA(cudaEventRecord(W->ev0, W->cin));
+  TF_CUDA(cudaStreamWaitEvent(s, W->ev0, 0));
+  TF_CUDA(cudaEventRecord(W->ev1, W->cout));
+  TF_CUDA(cudaStreamWaitEvent(s, W->ev1, 0));
   TF_CUDA(cudaStreamSynchronize(s));
   return 0;
 }
@@ -1247,7 +1398,8 @@ void tile_finalize(void) {
   std::lock_guard<std::recursive_mutex> lk(g_mu);
   for (auto& kv : g_ws) {
     Workspace& W = kv.second;
-    for (Buf* b : {&W.state, &W.q, &W.vx, &W.scratch, &W.info, &W.trace, &W.xt, &W.hostA, &W.hostAux, &W.hostPiv})
+    for (Buf* b : {&W.state, &W.q, &W.vx, &W.scratch, &W.info, &W.trace, &W.xt, &W.hostA, &W.hostAux, &W.hostPiv,
+                   &W.flags})
       release(*b);
   }
   g_ws.clear();

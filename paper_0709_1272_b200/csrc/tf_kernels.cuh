@@ -68,7 +68,6 @@ struct Ctx {
   }
 
 using GemmNT128 = Gemm<128, 128, 4, 4, false, false>;
-using GemmNT128N = Gemm<128, 128, 4, 4, false, false, true>;  // C preloaded, acc -= A B^T
 using GemmNT32 = Gemm<128, 32, 8, 2, false, false>;
 using GemmW64 = Gemm<64, 64, 4, 4, true, true>;
 using GemmW32 = Gemm<32, 128, 2, 8, true, true>;
@@ -352,10 +351,11 @@ __device__ inline void syrk_body(const Ctx& cx, const double* A, double* C, int 
   const int ni = rem;  // mi >= ni
   const int m0 = mi * RB, n0 = ni * RB;
   const int mm = min(RB, b - m0), nn = min(RB, b - n0);
-  GemmNT128N g;
-  g.load_acc(C + m0 + (size_t)n0 * b, b, mm, nn);
+  prefetch_l2(C + m0 + (size_t)n0 * b, b, mm, nn);
+  GemmNT128 g;
+  g.zero();
   g.run(sm, A + m0, b, A + n0, b, mm, nn, b);
-  g.store_acc(C + m0 + (size_t)n0 * b, b, mm, nn, /*mask=*/mi == ni, m0, n0);
+  sub_store(g, C + m0 + (size_t)n0 * b, b, mm, nn, /*lower_mask=*/mi == ni, m0, n0, /*red=*/true);
 }
 
 // GEMM (DGSMM with i > j): sub-tile `item` of C -= A B^T.
@@ -374,23 +374,21 @@ __device__ inline void gemm_body(const Ctx& cx, const double* A, const double* B
       const int n = (nj * gs + x) * RB;
       prefetch_l2(C + m0 + (size_t)n * b, b, mm, min(RB, b - n));
     }
-    // C preloaded into the accumulators (acc = C - A B^T): the epilogue is stores only
-    GemmNT128N g;
-    const int nn0 = min(RB, b - nj * gs * RB);
-    g.load_acc(C + m0 + (size_t)nj * gs * RB * b, b, mm, nn0);
-    g.run(sm, A + m0, b, B + (size_t)nj * gs * RB, b, mm, nn0, b);
+    GemmNT128 g;
+    g.zero();
+    g.run(sm, A + m0, b, B + (size_t)nj * gs * RB, b, mm, min(RB, b - nj * gs * RB), b);
     for (int x = 0; x < gs; ++x) {
       const int n = (nj * gs + x) * RB, nn = min(RB, b - n);
       if (x + 1 < gs) {
         const int n2 = n + RB, nn2 = min(RB, b - n2);
-        GemmNT128N h;
+        GemmNT128 h;
         h.prefill(sm, A + m0, b, B + n2, b, mm, nn2, b);
-        g.store_acc(C + m0 + (size_t)n * b, b, mm, nn, false, 0, 0);
-        g.load_acc(C + m0 + (size_t)n2 * b, b, mm, nn2);
+        sub_store(g, C + m0 + (size_t)n * b, b, mm, nn, false, 0, 0, /*red=*/true);
+        g.zero();
         g.pbase = h.pbase;
         g.finish(sm, A + m0, b, B + n2, b, mm, nn2, b);
       } else {
-        g.store_acc(C + m0 + (size_t)n * b, b, mm, nn, false, 0, 0);
+        sub_store(g, C + m0 + (size_t)n * b, b, mm, nn, false, 0, 0, /*red=*/true);
       }
     }
     __syncthreads();
@@ -402,12 +400,13 @@ __device__ inline void gemm_body(const Ctx& cx, const double* A, const double* B
 #ifdef TF_PROBE
   unsigned long long t0 = probe_now();
 #endif
-  GemmNT128N g;
-  g.load_acc(C + m0 + (size_t)n0 * b, b, mm, nn);
+  prefetch_l2(C + m0 + (size_t)n0 * b, b, mm, nn);
+  GemmNT128 g;
+  g.zero();
   TF_PROBE_MARK(0, t0);
   g.run(sm, A + m0, b, B + n0, b, mm, nn, b);
   TF_PROBE_MARK(1, t0);
-  g.store_acc(C + m0 + (size_t)n0 * b, b, mm, nn, false, 0, 0);
+  sub_store(g, C + m0 + (size_t)n0 * b, b, mm, nn, false, 0, 0, /*red=*/true);
   __syncthreads();
   TF_PROBE_MARK(2, t0);
 }

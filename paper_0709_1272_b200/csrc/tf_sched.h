@@ -38,6 +38,10 @@ constexpr int K_UNITL = 14, K_XGESSM = 15, K_XSSSSM = 16, K_XLARFB = 17, K_XSSRF
 // DAG algorithms: 0 chol, 1 qr, 2 lu (factorizations); 3 getrs (X <- A^{-1} X with LU
 // factors), 4 ormqr (X <- Q^T X), 5 qrs (X <- R^{-1} Q^T X), 6 lu_apply_N (X <- N X)
 constexpr int ALG_GETRS = 3, ALG_ORMQR = 4, ALG_QRS = 5, ALG_LUN = 6;
+// host <-> device overlap (tile_factor_host): ARRIVE(j) is completed by the scheduler when
+// tile column j has been copied in (a flag written by the copy stream); DONE(j) runs when
+// every tile of column j is final and sets the flag the D2H copy stream waits on
+constexpr int K_ARRIVE = 23, K_DONE = 24;
 
 TF_HD inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -111,6 +115,11 @@ struct Sched {
   int* exit_count;
   long long* trace;  // 5 per item or null
   int trace_cap;
+  // copy overlap (0 / null unless the DAG has ARRIVE / DONE tasks)
+  const int* arrive_flags;  // [narrive], set to 1 by the H2D copy stream after tile column j
+  int* arrive_next;         // next column whose ARRIVE task is still pending
+  int arrive_task0, narrive;
+  int* done_flags;          // [narrive], set to 1 by DONE(j)
 };
 
 // One remote push: when a SEND task completes, item `item` (the consumer's RECV task)

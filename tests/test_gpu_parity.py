@@ -208,3 +208,44 @@ def test_lu_singular_info(n, b, ib, col):
     _, _, _, gi = gpu_factor("lu", A, b, ib)
     _, _, _, oi = oracle_factor("lu", A, b, ib)
     assert gi == oi == col + 1
+
+
+# ------------------------------------------------------------------ end-to-end host path
+
+@pytest.mark.parametrize("alg,n,b,ib", [("chol", 1024, 128, 32), ("qr", 1024, 256, 32), ("lu", 1024, 256, 32),
+                                        ("chol", 1536, 512, 64)])
+def test_factor_host_overlapped_equals_device(alg, n, b, ib):
+    """tile_factor_host streams tile columns in / out while the factorization runs
+    (ARRIVE / DONE tasks in the DAG); the factors are bitwise those of the device call."""
+    A = {"chol": tilegen.spd, "qr": tilegen.uniform, "lu": tilegen.normal}[alg](n, 13)
+    G, GA, GP, gi = gpu_factor(alg, A, b, ib)
+    hA = gpu_pack(A, b).cpu().pin_memory()
+    if alg == "chol":
+        # upper tiles are neither read nor written: start them at NaN to prove it
+        p = n // b
+        v = hA.view(p * p, b * b)
+        for j in range(p):
+            for i in range(j):
+                v[i + j * p] = float("nan")
+    hAux = torch.zeros(tf.tile_qr_t_elems(n, b, ib), dtype=torch.float64).pin_memory() if alg != "chol" else None
+    hPiv = torch.zeros(tf.tile_lu_ipiv_elems(n, b), dtype=torch.int32).pin_memory() if alg == "lu" else None
+    hInfo = torch.full((1,), 77, dtype=torch.int32)
+    tf.tile_factor_host(alg, n, b, ib, hA, hAux, hPiv, hInfo)
+    assert int(hInfo.item()) == 0 == gi
+    H = hA.numpy()
+    if alg == "chol":
+        p = n // b
+        L1, L2 = oracle.tile_lower_L(H, n, b), oracle.tile_lower_L(G, n, b)
+        assert np.array_equal(L1, L2)
+    else:
+        assert np.array_equal(H, G)
+        p = n // b
+        for k in range(p):
+            for i in range(k if alg == "qr" else k + 1, p):  # T strips i >= k, L strips i > k
+                o = (i + k * p) * ib * b
+                assert np.array_equal(hAux.numpy()[o:o + ib * b], GA[o:o + ib * b]), (i, k)
+        if alg == "lu":
+            for k in range(p):
+                for i in range(k, p):
+                    o = (i + k * p) * b
+                    assert np.array_equal(hPiv.numpy()[o:o + b], GP[o:o + b]), (i, k)

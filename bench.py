@@ -41,6 +41,8 @@ CONFIGS = {
     3: dict(kind="lu", n=4096, b=256, ib=32, gen="normal", desc="config3: tiled LU (incremental pivoting) FP64 n=4096 b=256 ib=32, A~N(0,1)"),
     4: dict(kind="chol", n=32768, b=512, ib=64, gen="spd", desc="config4: tiled Cholesky FP64 n=32768 b=512, SPD A=MM^T/n+nI, M~U[-1,1]"),
     5: dict(kind="qr", n=32768, b=512, ib=64, gen="uniform", desc="config5: tiled QR FP64 n=32768 b=512 ib=64, A~U[-0.5,0.5]"),
+    # the third algorithm at the scale of configs 4-5 (not a BASELINE config)
+    6: dict(kind="lu", n=32768, b=512, ib=64, gen="normal", desc="NEXT-1: tiled LU (incremental pivoting) FP64 n=32768 b=512 ib=64, A~N(0,1)"),
 }
 METRIC = "FP64 GFLOP/s and % of FP64 tensor peak per factorization at 1/2/4/8 B200"
 L2_BYTES = 126 * 2**20
@@ -491,7 +493,7 @@ def run_ours(args, rank, world, local_rank):
     per = []
     if not args.only and rank == 0 and world == 1:
         for c in sorted(CONFIGS):
-            if c == args.config:
+            if c == args.config or c == 6:  # config 6 (NEXT-1) runs with --config 6
                 continue
             cc = CONFIGS[c]
             r, _ = run_device(tf, torch, cc, 3, 3, check=False)

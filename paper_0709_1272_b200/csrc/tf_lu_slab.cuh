@@ -83,19 +83,53 @@ __device__ long long g_lu_prof[24];  // 12-15: lu_panel phases (argmax, barrier,
 // content of the previous top row that named the same bottom row (or of that bottom row if
 // none), and a named bottom row ends with the last top row that named it.  Each column then
 // gathers in two shared-memory round trips instead of a 32-step dependent chain.
+// Blocks applied in sequence double-buffer their inputs: while block s runs, the U rows,
+// the L-strip block and the pivots of block s+1 land in the other buffer set by cp.async
+// (LuBlk next), so only the first block of a sequence waits for its loads.
+struct LuBlk {
+  const double* Us;   // U rows of the block (slab columns), ld b
+  const double* Lsb;  // L-strip block, ld ldl
+  const int* pv;      // pivots
+  int ib, ldl;
+};
+constexpr int LU_SETW = 64 * LU_LDW + 64 * 65 + 32;  // one buffer set: sU, sL, pivots (doubles)
+__device__ __forceinline__ double* lu_set(double* sm, int buf) {
+  // [sA | flag/srcT/lastS ints | set 0 | set 1]
+  return sm + 64 * LU_LDW + 384 + buf * LU_SETW;
+}
+template <int IB>
+__device__ __forceinline__ void lu_ts_prefetch(const LuBlk& nx, int b, double* set) {
+  double* sU = set;
+  double* sL = sU + 64 * LU_LDW;
+  int* spv = reinterpret_cast<int*>(sL + 64 * 65);
+  const int tid = threadIdx.x;
+  for (int e = tid; e < IB * NSR; e += TF_THREADS) {
+    const int m = e % IB, c = e / IB;
+    cp_async8(sU + m * LU_LDW + c, nx.Us + m + (size_t)c * b, 8);
+  }
+  for (int e = tid; e < IB * IB; e += TF_THREADS) {
+    const int r = e % IB, m = e / IB;
+    const double* src = nx.Lsb + r + (size_t)m * nx.ldl;
+    cp_async8(sL + r * (IB + 1) + m, r > m ? src : nx.Lsb, r > m ? 8 : 0);  // zero-fill r <= m
+  }
+  if (tid < IB) asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(spv + tid)), "l"(nx.pv + tid));
+  cp_async_commit();
+}
+
 template <int MI, int IB>
 __device__ __forceinline__ void lu_ts_apply_t(double (&acc)[MI][SNJ][2], double* Us, const double* Lc,
-                                              const double* Lsb, const int* pv, int ldl, int b, double* sm) {
+                                              const LuBlk& cur, int b, double* sm, int buf, bool pre,
+                                              const LuBlk* nx) {
   constexpr int RW = 8 * MI;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   const int r0 = warp * RW;
-  double* sU = sm;                              // IB x LU_LDW: U_s
-  double* sA = sU + 64 * LU_LDW;                // IB slots x LU_LDW: the A rows the pivots name
-  double* sL = sA + 64 * LU_LDW;                // IB x (IB+1): L(r, m), r > m
-  int* flag = reinterpret_cast<int*>(sL + 64 * 65);  // b: slot of bottom row r (INT_MAX = none)
-  int* spv = flag + 512;                        // IB pivots of the block
-  int* srcT = spv + 64;                         // top row P <- top row srcT (< 64) or slot srcT - 64
+  double* sA = sm;                              // IB slots x LU_LDW: the A rows the pivots name
+  int* flag = reinterpret_cast<int*>(sA + 64 * LU_LDW);  // b: slot of bottom row r (INT_MAX = none)
+  int* srcT = flag + 512;                       // top row P <- top row srcT (< 64) or slot srcT - 64
   int* lastS = srcT + 64;                       // [half][slot]: the slot <- top row lastS (-1: kept)
+  double* sU = lu_set(sm, buf);                 // IB x LU_LDW: U_s
+  double* sL = sU + 64 * LU_LDW;                // IB x (IB+1): L(r, m), r > m
+  int* spv = reinterpret_cast<int*>(sL + 64 * 65);  // IB pivots of the block
   // the L columns of the update, in flight from the start (they are this block's own
   // results, L2-resident): MI * IB/4 values per thread
   constexpr int NPRE = (MI * IB / 4 <= 16) ? IB / 4 : 0;
@@ -106,15 +140,10 @@ __device__ __forceinline__ void lu_ts_apply_t(double (&acc)[MI][SNJ][2], double*
 #pragma unroll
     for (int i = 0; i < MI; ++i) la[ks][i] = -Lc[(r0 + 8 * i + g) + (size_t)(4 * ks + q) * b];
   for (int r = tid; r < b; r += TF_THREADS) flag[r] = INT_MAX;
-  if (tid < IB) spv[tid] = pv[tid];
-  for (int e = tid; e < IB * NSR; e += TF_THREADS) {
-    const int m = e % IB, c = e / IB;
-    sU[m * LU_LDW + c] = ldg_cg(Us + m + (size_t)c * b);
-  }
-  for (int e = tid; e < IB * IB; e += TF_THREADS) {
-    const int r = e % IB, m = e / IB;
-    sL[r * (IB + 1) + m] = (r > m) ? ldg_cg(Lsb + r + (size_t)m * ldl) : 0.0;
-  }
+  // this block's inputs: requested now, or by the previous block's call (the only cp.async
+  // group in flight at this point; the next block's is issued after the solve below)
+  if (!pre) lu_ts_prefetch<IB>(cur, b, sU);
+  cp_async_wait<0>();
   __syncthreads();
   TF_LU_T(16);
   if (tid < IB) {
@@ -178,6 +207,11 @@ __device__ __forceinline__ void lu_ts_apply_t(double (&acc)[MI][SNJ][2], double*
   }
   __syncthreads();
   TF_LU_T(18);
+  // the next block's inputs into the other buffer set while this one finishes
+  if (nx) {
+    if (nx->ib == 32) lu_ts_prefetch<32>(*nx, b, lu_set(sm, buf ^ 1));
+    else lu_ts_prefetch<64>(*nx, b, lu_set(sm, buf ^ 1));
+  }
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
     const int f = flag[r0 + 8 * i + g];
@@ -192,12 +226,21 @@ __device__ __forceinline__ void lu_ts_apply_t(double (&acc)[MI][SNJ][2], double*
     Us[m + (size_t)c * b] = sU[m * LU_LDW + c];
   }
   TF_LU_T(19);
-  // A -= L[:, block] U_s
+  // A -= L[:, block] U_s (L operand one k-step ahead when it is not preloaded)
+  double an[MI];
+  if (!NPRE) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i) an[i] = -Lc[(r0 + 8 * i + g) + (size_t)q * b];
+  }
 #pragma unroll
   for (int ks = 0; ks < IB / 4; ++ks) {
     double a[MI], bq[SNJ];
 #pragma unroll
-    for (int i = 0; i < MI; ++i) a[i] = NPRE ? la[NPRE ? ks : 0][i] : -Lc[(r0 + 8 * i + g) + (size_t)(4 * ks + q) * b];
+    for (int i = 0; i < MI; ++i) a[i] = NPRE ? la[NPRE ? ks : 0][i] : an[i];
+    if (!NPRE && ks + 1 < IB / 4) {
+#pragma unroll
+      for (int i = 0; i < MI; ++i) an[i] = -Lc[(r0 + 8 * i + g) + (size_t)(4 * (ks + 1) + q) * b];
+    }
 #pragma unroll
     for (int j = 0; j < SNJ; ++j) bq[j] = sU[(4 * ks + q) * LU_LDW + 8 * j + g];
 #pragma unroll
@@ -209,11 +252,15 @@ __device__ __forceinline__ void lu_ts_apply_t(double (&acc)[MI][SNJ][2], double*
   TF_LU_T(20);
 }
 
+// Apply `cur` (buffer set `buf`; pre = its inputs were already requested by the previous
+// call), prefetching `nx` (may be null) into the other set.  Returns the next buffer set.
 template <int MI>
-__device__ __forceinline__ void lu_ts_apply(double (&acc)[MI][SNJ][2], double* Us, const double* Lc, const double* Lsb,
-                                            const int* pv, int ib, int ldl, int b, double* sm) {
-  if (ib == 32) lu_ts_apply_t<MI, 32>(acc, Us, Lc, Lsb, pv, ldl, b, sm);
-  else lu_ts_apply_t<MI, 64>(acc, Us, Lc, Lsb, pv, ldl, b, sm);
+__device__ __forceinline__ int lu_ts_apply(double (&acc)[MI][SNJ][2], double* Us, const double* Lc,
+                                           const LuBlk& cur, int b, double* sm, int buf, bool pre,
+                                           const LuBlk* nx) {
+  if (cur.ib == 32) lu_ts_apply_t<MI, 32>(acc, Us, Lc, cur, b, sm, buf, pre, nx);
+  else lu_ts_apply_t<MI, 64>(acc, Us, Lc, cur, b, sm, buf, pre, nx);
+  return buf ^ 1;
 }
 
 // SSSSM item: 32 columns of [U_kj; A_ij].  L = A_ik (multipliers), Ls = L strip (i,k),
@@ -226,8 +273,12 @@ __device__ inline void ssssm_reg(const Ctx& cx, const double* L, const double* L
   A += (size_t)item * NSR * b;
   double acc[MI][SNJ][2];
   slab_load<MI>(acc, A, b);
-  for (int c0 = 0; c0 < b; c0 += ib)
-    lu_ts_apply<MI>(acc, U + c0, L + (size_t)c0 * b, Ls + (size_t)c0 * ib, ipiv + c0, ib, ib, b, sm);
+  int buf = 0;
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    const LuBlk cur{U + c0, Ls + (size_t)c0 * ib, ipiv + c0, ib, ib};
+    const LuBlk nxt{U + c0 + ib, Ls + (size_t)(c0 + ib) * ib, ipiv + c0 + ib, ib, ib};
+    buf = lu_ts_apply<MI>(acc, U + c0, L + (size_t)c0 * b, cur, b, sm, buf, c0 > 0, c0 + ib < b ? &nxt : nullptr);
+  }
   slab_store<MI>(acc, A, b);
 }
 
@@ -520,12 +571,22 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
   for (int cs = 0; cs < b; cs += NSR) {
     const int s0 = cs - cs % ib, off = cs - s0;  // this slab's inner block and its offset in it
     slab_load<MI>(acc, A + (size_t)cs * b, b);
-    for (int c0 = 0; c0 < s0; c0 += ib)
-      lu_ts_apply<MI>(acc, U + c0 + (size_t)cs * b, A + (size_t)c0 * b, Ls + (size_t)c0 * ib, ipiv + c0, ib, ib, b,
-                      sm);
-    if (off)  // the block's first slab, as a 32-column sub-block
-      lu_ts_apply<MI>(acc, U + s0 + (size_t)cs * b, A + (size_t)s0 * b, Ls + (size_t)s0 * ib, ipiv + s0, NSR, ib, b,
-                      sm);
+    {
+      // the finished inner blocks, then (second slab of a 64-block) the block's first slab
+      // as a 32-column sub-block; each block's inputs prefetched during the previous one
+      int buf = 0;
+      const int nfull = s0 / ib, nblk = nfull + (off ? 1 : 0);
+      auto blk = [&](int x) {
+        const int c0 = x < nfull ? x * ib : s0;
+        return LuBlk{U + c0 + (size_t)cs * b, Ls + (size_t)c0 * ib, ipiv + c0, x < nfull ? ib : NSR, ib};
+      };
+      for (int x = 0; x < nblk; ++x) {
+        const LuBlk cur = blk(x), nxt = blk(x + 1 < nblk ? x + 1 : x);
+        const int c0 = x < nfull ? x * ib : s0;
+        buf = lu_ts_apply<MI>(acc, U + c0 + (size_t)cs * b, A + (size_t)c0 * b, cur, b, sm, buf, x > 0,
+                              x + 1 < nblk ? &nxt : nullptr);
+      }
+    }
     TF_LU_T(8);
     double* P = sm;
     double* UL = P + 32 * ldp;

@@ -119,6 +119,8 @@ CASES = [
     ("lu", 1024, 128, 32, 1, 2),
     ("lu", 1152, 128, 32, 1, 4),
     ("lu", 4096, 256, 32, 1, 2),     # config 3 sizes
+    ("lu", 2048, 512, 64, 1, 2),     # NEXT-1 tile shape (b = 512, ib = 64), p = 4
+    ("qr", 2048, 512, 64, 1, 2),     # config-5 tile shape
 ]
 
 

@@ -135,3 +135,78 @@ def test_config5_qr_full_residual_and_orthogonality():
     print(f"[config 5] est ||A - QR||_F/||A||_F = {res:.3e}, est ||Q^T Q - I||_F = {orth:.3e}")
     assert res <= 1e-13, res
     assert orth <= 1e-13 * n, orth
+
+
+def test_config6_lu_full_residual_and_solve():
+    """NEXT-1 (Alg. 3 at n = 32768, b = 512, ib = 64, the launch bench.py --config 6 times):
+    the oracle cannot factor it in test time, so properties that hold at any size are checked:
+    every stored multiplier |l| <= 1 (GETWP's pivots always eliminate with the
+    larger element), ||A - N U||_F / ||A||_F estimated with Gaussian probes (N applied with
+    the GPU's tile_lu_apply_N, itself parity-tested against the oracle), and the backward
+    error of a solve with tile_getrs."""
+    n, b, ib = 32768, 512, 64
+    dense = tilegen.normal_torch(n, 0, torch.device("cuda"))   # row-major buffer = A^T
+    T = torch.empty(n * n, dtype=torch.float64, device="cuda")
+    tf.tile_pack(n, n, b, dense.view(-1), T)
+    Ls = torch.zeros(tf.tile_lu_l_elems(n, b, ib), dtype=torch.float64, device="cuda")
+    piv = torch.zeros(tf.tile_lu_ipiv_elems(n, b), dtype=torch.int32, device="cuda")
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    tf.tile_lu(n, b, ib, T, Ls, piv, info)
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    D = torch.empty(n * n, dtype=torch.float64, device="cuda")
+    tf.tile_unpack(n, n, b, T, D)
+    F = D.view(n, n).t()                                       # the factored matrix, (row, col)
+    assert float(torch.tril(F, -1).abs().max()) <= 1.0
+    assert float(Ls.abs().max()) <= 1.0
+    U = torch.triu(F)
+    del D
+    A = dense.t()
+    g = torch.Generator(device="cuda").manual_seed(11)
+    X = torch.randn(n, 4, dtype=torch.float64, device="cuda", generator=g)
+    Y = (U @ X).t().contiguous()                               # (4, n) = column-major n x 4
+    tf.tile_lu_apply_N(n, b, ib, T, Ls, piv, Y)
+    E = A @ X - Y.t()
+    res = float(torch.linalg.norm(E) / (2.0 * torch.linalg.norm(A)))
+    print(f"[config 6] est ||A - NU||_F/||A||_F = {res:.3e}")
+    # GETWP's factorization error grows with p and n (the lab: 1.5e-14 at p = 1 to 1.2e-12 at
+    # p = 128 for n = 2048; test_config6_method_level pins GPU = oracle level at p = 16 with
+    # this tile shape); no oracle value exists at n = 32768, so this is a sanity bound that a
+    # wrong elimination (O(1) errors) cannot pass, and the strong check is the solve below
+    assert res <= 1e-8, res
+    y = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    x = y.clone()
+    tf.tile_getrs(n, b, ib, T, Ls, piv, x)
+    be = float((y - A @ x).abs().max() / (torch.linalg.matrix_norm(A, ord=float("inf")) * x.abs().max()))
+    print(f"[config 6] solve backward error = {be:.3e}")
+    assert be <= 1e-12, be
+
+
+def test_config6_method_level_p16():
+    """The b = 512 / ib = 64 LU path at p = 16 (n = 8192): the GPU's ||A - N U||_F / ||A||_F
+    is at the oracle's own level (<= max(1e-12, 2x the oracle's), BASELINE's LU residual
+    reading Z14); the oracle runs on all host cores (its thread-pool executor, bitwise equal
+    to the sequential driver).  Pivots are NOT required to agree here: at this depth the
+    oracle's own rounding spread exceeds some pivot gaps (seed 3: first disagreement at tile
+    (14,12) column 337, winner / runner-up |x| 6.0839512 / 6.0839224, relative gap 4.7e-6,
+    C5 pivot margin 0.24 — a pivot-fragile seed under reading C5, diagnosed with
+    tools/lu_pivot_diag.py); both factorizations are valid GETWP runs, and the bit-exact
+    pivot requirement is carried by the certified seeds of test_gpu_parity / config 3."""
+    n, b, ib = 8192, 512, 64
+    A = tilegen.normal(n, 3)
+    G, GL, Gp, gi = gpu_factor("lu", A, b, ib)
+    import os
+    F = oracle.pack(A, b)
+    OL, Op, oi = oracle.factor_par("lu", F, n, b, ib, len(os.sched_getaffinity(0)))
+    assert gi == oi == 0
+    p = n // b
+    same = sum(np.array_equal(Gp[(i + k * p) * b:(i + k * p + 1) * b], Op[(i + k * p) * b:(i + k * p + 1) * b])
+               for k in range(p) for i in range(k, p))
+    print(f"[n=8192 b=512 ib=64] identical pivot vectors: {same} of {p * (p + 1) // 2}")
+    # ||A - N U||_F estimated with the same 8 Gaussian probes for both (E||EX||^2 = k||E||^2)
+    X = np.asfortranarray(np.random.default_rng(8).standard_normal((n, 8)))
+    AX, nA = A @ X, np.linalg.norm(A) * 8 ** 0.5
+    rg = np.linalg.norm(AX - oracle.lu_apply_N(G, GL, Gp, oracle.lu_U(G, n, b) @ X, n, b, ib)) / nA
+    ro = np.linalg.norm(AX - oracle.lu_apply_N(F, OL, Op, oracle.lu_U(F, n, b) @ X, n, b, ib)) / nA
+    print(f"[n=8192 b=512 ib=64] est ||A - NU||_F/||A||_F: gpu {rg:.3e} oracle {ro:.3e}")
+    assert rg <= max(1e-12, 2 * ro), (rg, ro)

@@ -18,7 +18,8 @@ using namespace tf;
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
 
 __global__ void __launch_bounds__(TF_THREADS, 1)
-kb_kernel(int kind, int b, int ib, double* tiles, double* aux, int* ipiv, double* scratch, size_t scr, int reps) {
+kb_kernel(int kind, int b, int ib, double* tiles, double* aux, int* ipiv, double* scratch, size_t scr, int reps,
+          int shared_ab) {
   extern __shared__ __align__(16) double sm[];
   Ctx cx;
   cx.b = b; cx.ib = ib; cx.scratch = scratch + (size_t)blockIdx.x * scr; cx.info = nullptr; cx.abort_flag = nullptr;
@@ -27,6 +28,10 @@ kb_kernel(int kind, int b, int ib, double* tiles, double* aux, int* ipiv, double
   double* t0 = tiles + (size_t)blockIdx.x * 3 * bb;
   double* t1 = t0 + bb;
   double* t2 = t1 + bb;
+  if (shared_ab) {  // every CTA reads the same two operand tiles (L2-resident), own output tile
+    t0 = tiles;
+    t1 = tiles + bb;
+  }
   double* ax = aux + (size_t)blockIdx.x * ib * b;
   int* pv = ipiv + (size_t)blockIdx.x * b;
   const int nit = items_of(kind, b, ib);
@@ -99,6 +104,7 @@ int main(int argc, char** argv) {
   const int b = atoi(argv[2]), ib = atoi(argv[3]);
   const int cps = argc > 4 ? atoi(argv[4]) : 1;
   const int reps = argc > 5 ? atoi(argv[5]) : 4;
+  const int shared_ab = argc > 6 ? atoi(argv[6]) : 0;
   int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int grid = kind == 0 || kind == 4 || kind == 6 || kind == 8 || kind == 10 ? sms * cps : sms * cps;
   const size_t bb = (size_t)b * b;
@@ -116,11 +122,11 @@ int main(int argc, char** argv) {
   CK(cudaFuncSetAttribute(kb_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_DOUBLES * 8));
   init_kernel<<<1024, 256>>>(tiles, grid * 3 * bb, b, kind);
   CK(cudaDeviceSynchronize());
-  kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, 1);
+  kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, 1, shared_ab);
   CK(cudaDeviceSynchronize());
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps);
+  kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps, shared_ab);
   cudaEventRecord(e1);
   CK(cudaEventSynchronize(e1));
   float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -130,7 +136,7 @@ int main(int argc, char** argv) {
     cudaMallocManaged(&pr, 8 * sizeof(unsigned long long));
     for (int i = 0; i < 8; ++i) pr[i] = 0;
     cudaMemcpyToSymbol(g_probe, &pr, sizeof(pr));
-    kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps);
+    kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps, shared_ab);
     CK(cudaDeviceSynchronize());
     printf("probe us/item:");
     for (int i = 0; i < 8; ++i) printf(" [%d] %.2f", i, pr[i] / 1e3 / grid / reps);
@@ -141,7 +147,7 @@ int main(int argc, char** argv) {
   {
     long long z[24] = {0}, h[24];
     cudaMemcpyToSymbol(g_lu_prof, z, sizeof(z));
-    kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps);
+    kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps, shared_ab);
     CK(cudaDeviceSynchronize());
     cudaMemcpyFromSymbol(h, g_lu_prof, sizeof(h));
     printf("lu phases us/task:");

@@ -718,6 +718,8 @@ TF_DEF_VARIANT(v_larfb_reg, larfb_reg, (Ctx cx, const double* VX, const double* 
                (cx, VX, Tst, C, item, dsm))
 TF_DEF_VARIANT(v_ssrfb_reg, ssrfb_reg, (Ctx cx, const double* V, const double* Tst, double* R, double* A, int item),
                (cx, V, Tst, R, A, item, dsm))
+TF_DEF_VARIANT(v_ssrfb_mirror, ssrfb_mirror,
+               (Ctx cx, const double* V, const double* Tst, double* R, double* A, int item), (cx, V, Tst, R, A, item, dsm))
 TF_DEF_REF(v_geqrt_ref, geqrt_ref, (Ctx cx, double* A, double* Tst, double* VX), (cx, A, Tst, VX, dsm))
 TF_DEF_REF(v_larfb_ref, larfb_ref, (Ctx cx, const double* VX, const double* Tst, double* C, int item),
            (cx, VX, Tst, C, item, dsm))
@@ -744,7 +746,11 @@ __device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* T
 // SSRFB: slab `item` of [R_kj; A_ij] <- Q_ik^T [R_kj; A_ij].
 __device__ inline void ssrfb_item(const Ctx& cx, const double* V, const double* Tst, double* R, double* A,
                                   int item, double* sm) {
+#ifdef TF_SSRFB_SLAB
   if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_ssrfb_reg, cx, V, Tst, R, A, item);
+#else
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_ssrfb_mirror, cx, V, Tst, R, A, item);
+#endif
   else v_ssrfb_ref(cx, V, Tst, R, A, item);
 }
 

@@ -56,21 +56,6 @@ __device__ __forceinline__ void lu_block_solve(double* sU, const double* sL, int
   __syncwarp();
 }
 
-#ifdef TF_PROF_LU
-__device__ long long g_lu_prof[24];  // 12-15: lu_panel phases (argmax, barrier, merge, update); 16-20: lu_ts_apply
-#define TF_LU_T0() long long lu_t_ = clock64()
-#define TF_LU_T(k)                                                       \
-  do {                                                                   \
-    if (threadIdx.x == 0) {                                              \
-      const long long t_ = clock64();                                    \
-      atomicAdd(reinterpret_cast<unsigned long long*>(&g_lu_prof[k]), (unsigned long long)(t_ - lu_t_)); \
-      lu_t_ = t_;                                                        \
-    }                                                                    \
-  } while (0)
-#else
-#define TF_LU_T0() (void)0
-#define TF_LU_T(k) (void)0
-#endif
 
 // One inner block of the pairwise-pivoted update on a register slab (SSSSM step):
 // [U_s; A] <- swaps of block s, U_s <- (I + Ls_s)^{-1} U_s, A -= L[:, s] U_s.

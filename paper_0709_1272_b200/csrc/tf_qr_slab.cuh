@@ -24,6 +24,23 @@
 
 namespace tf {
 
+// Phase probes (tools/kbench built with -DTF_PROF_LU): thread 0 accumulates clock64 deltas.
+#ifdef TF_PROF_LU
+__device__ long long g_lu_prof[32];  // 12-15: lu_panel phases (argmax, barrier, merge, update); 16-20: lu_ts_apply; 24-28: slab_apply (QR)
+#define TF_LU_T0() long long lu_t_ = clock64()
+#define TF_LU_T(k)                                                       \
+  do {                                                                   \
+    if (threadIdx.x == 0) {                                              \
+      const long long t_ = clock64();                                    \
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g_lu_prof[k]), (unsigned long long)(t_ - lu_t_)); \
+      lu_t_ = t_;                                                        \
+    }                                                                    \
+  } while (0)
+#else
+#define TF_LU_T0() (void)0
+#define TF_LU_T(k) (void)0
+#endif
+
 constexpr int SNJ = NSR / 8;            // n-blocks of a 32-column slab
 constexpr int SLDW = NSR + 4;           // W / W2 row stride in smem (conflict-free B fragments)
 constexpr int SLDC = 64 + 2;            // column stride of the T and R blocks in smem
@@ -58,6 +75,7 @@ __device__ __forceinline__ void slab_apply(double (&acc)[MI][SNJ][2], const doub
     }
   }
   cp_async_commit();
+  TF_LU_T0();
   // B fragments (row 4*ks + q, column 8*j + g of the warp's rows) from the accumulators:
   // k-steps 2i, 2i+1 of accumulator block i in two 64-bit shuffle rounds
   const int src = 4 * q + (g >> 1);
@@ -119,8 +137,10 @@ __device__ __forceinline__ void slab_apply(double (&acc)[MI][SNJ][2], const doub
     if (pp == np - 1) cp_async_wait<0>();
     __syncthreads();
   }
+  TF_LU_T(24);
   reduce(nw - 16, part + ((np - 1) & 1) * SPB);
   __syncthreads();
+  TF_LU_T(25);
   // ---- W2 = T^T (R_s + W): T^T lower triangular -> block (mi, j) needs k < 8(mi+1)
   {
     const int bpw = nw / 32;  // 8x8 output blocks per warp (1 or 2), same mi
@@ -152,6 +172,7 @@ __device__ __forceinline__ void slab_apply(double (&acc)[MI][SNJ][2], const doub
     }
   }
   __syncthreads();
+  TF_LU_T(26);
   // ---- A -= V W2
   if (active) {
     for (int ks = 0; ks < nw / 4; ++ks) {
@@ -166,7 +187,9 @@ __device__ __forceinline__ void slab_apply(double (&acc)[MI][SNJ][2], const doub
         for (int j = 0; j < SNJ; ++j) dmma(acc[i][j], a[i], bq[j]);
     }
   }
+  TF_LU_T(27);
   __syncthreads();  // sW2 / sT / sR / partials are rewritten by the next group
+  TF_LU_T(28);
 }
 
 template <int MI>
@@ -191,6 +214,171 @@ __device__ __forceinline__ void slab_store(const double (&acc)[MI][SNJ][2], doub
     for (int j = 0; j < SNJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) A[(r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * b] = acc[i][j][e];
+}
+
+// SSRFB with a shared-memory mirror of the slab (b <= 512).  The slab stays in the DMMA
+// accumulators for the A update (as in slab_apply), and a copy in shared memory (rows
+// swizzled so the W pass's B-fragment loads are conflict-free) feeds W = V_s^T A: the 16
+// warps form two groups that each reduce over half of the rows, every warp owning whole W
+// fragments over its group's rows, so W is ONE pass (per-warp K of b/2, no 16-way partial
+// reduction through shared memory and no barrier per 16 W rows), the two group partials are
+// added in a fixed order (group 0's + group 1's).  Then W2 = T_s^T (R_s + W) (DMMA),
+// R_s -= W2, A -= V_s W2 on the accumulators, and the mirror rows are refreshed.
+constexpr int MIR_LD = NSR;  // mirror row length (doubles), swizzled
+__device__ __forceinline__ int mir_idx(int r, int c) { return r * MIR_LD + (c ^ ((r & 3) << 2)); }
+
+template <int MI>
+__device__ inline void ssrfb_mirror(const Ctx& cx, const double* V, const double* Tst, double* R, double* A, int item,
+                                    double* sm) {
+  constexpr int RW = 8 * MI;
+  const int b = cx.b, ib = cx.ib;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
+  const int r0 = warp * RW;
+  R += (size_t)item * NSR * b;
+  A += (size_t)item * NSR * b;
+  double* sMir = sm;                        // b x 32 (swizzled)
+  double* sW = sMir + 512 * MIR_LD;         // 64 x SLDW: group-1 partials, then W, then W2
+  double* sR = sW + 64 * SLDW;              // R_s, column-major, ld SLDC
+  double* sT = sR + NSR * SLDC;             // T, column-major, ld SLDC
+  double acc[MI][SNJ][2];
+  slab_load<MI>(acc, A, b);
+  auto mirror = [&]() {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < SNJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) sMir[mir_idx(r0 + 8 * i + g, 8 * j + 2 * q + e)] = acc[i][j][e];
+  };
+  mirror();
+  const int grp = warp >> 3, wg = warp & 7;
+  const int kh = b / 2, k0g = grp * kh;     // this group's rows of the W reduction
+  for (int c0 = 0; c0 < b; c0 += ib) {
+    const int nw = ib;
+    const double* Vs = V + (size_t)c0 * b;
+    const double* Tb = Tst + (size_t)c0 * ib;
+    double* Rr = R + c0;
+    // T_s and R_s by cp.async while W is formed
+    for (int x = tid; x < nw * (nw / 2); x += TF_THREADS) {
+      const int c = x / (nw / 2), r = 2 * (x % (nw / 2));
+      cp_async16(sT + c * SLDC + r, Tb + (size_t)c * ib + r, 16);
+    }
+    for (int x = tid; x < NSR * (nw / 2); x += TF_THREADS) {
+      const int c = x / (nw / 2), r = 2 * (x % (nw / 2));
+      cp_async16(sR + c * SLDC + r, Rr + r + (size_t)c * b, 16);
+    }
+    cp_async_commit();
+    __syncthreads();  // the mirror holds this block's input slab
+    TF_LU_T0();
+    // ---- W (nw x 32) over this group's rows: warp wg owns m-block mb, n-blocks nb0 .. nb0+NB-1
+    constexpr int NBMAX = 4;
+    const int NB = nw == 64 ? 4 : 2;
+    const int mb = nw == 64 ? wg : (wg >> 1), nb0 = nw == 64 ? 0 : 2 * (wg & 1);
+    double w[NBMAX][2];
+#pragma unroll
+    for (int x = 0; x < NBMAX; ++x) w[x][0] = w[x][1] = 0.0;
+    const double* vcol = Vs + (size_t)(8 * mb + g) * b + k0g + q;  // V(k0g + 4ks + q, 8mb + g)
+    // V operand 8 k-steps at a time, the next group in flight while this one is used
+    double av[8], avn[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) avn[u] = vcol[4 * u];
+#pragma unroll 1
+    for (int ks0 = 0; ks0 < kh / 4; ks0 += 8) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) av[u] = avn[u];
+      if (ks0 + 8 < kh / 4) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) avn[u] = vcol[4 * (ks0 + 8 + u)];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0g + 4 * (ks0 + u) + q;
+#pragma unroll
+        for (int x = 0; x < NBMAX; ++x)
+          if (x < NB) dmma(w[x], av[u], sMir[mir_idx(k, 8 * (nb0 + x) + g)]);
+      }
+    }
+    TF_LU_T(24);
+    // group 1 -> shared memory, group 0 adds (fixed order: group 0 + group 1)
+    if (grp == 1) {
+#pragma unroll
+      for (int x = 0; x < NBMAX; ++x)
+        if (x < NB)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) sW[(8 * mb + g) * SLDW + 8 * (nb0 + x) + 2 * q + e] = w[x][e];
+    }
+    __syncthreads();
+    if (grp == 0) {
+#pragma unroll
+      for (int x = 0; x < NBMAX; ++x)
+        if (x < NB)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            double* p = sW + (8 * mb + g) * SLDW + 8 * (nb0 + x) + 2 * q + e;
+            *p = w[x][e] + *p;
+          }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    TF_LU_T(25);
+    // ---- W2 = T^T (R_s + W) on the DMMA pipe (T^T lower triangular: block mi needs k < 8(mi+1))
+    double c2[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const int bpw = nw / 32;
+    const int mi = warp / (SNJ / bpw), j0 = (warp % (SNJ / bpw)) * bpw;
+    {
+      const int nks = 2 * (mi + 1);
+      for (int ks = 0; ks < nks; ++ks) {
+        const int k = 4 * ks + q;
+        const double a = sT[(8 * mi + g) * SLDC + k];
+        const double b0 = sW[k * SLDW + 8 * j0 + g] + sR[(8 * j0 + g) * SLDC + k];
+        dmma(c2[0], a, b0);
+        if (bpw == 2) {
+          const double b1 = sW[k * SLDW + 8 * j0 + 8 + g] + sR[(8 * j0 + 8 + g) * SLDC + k];
+          dmma(c2[1], a, b1);
+        }
+      }
+    }
+    __syncthreads();  // every warp has read W: W2 overwrites it
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      if (x < bpw) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int m = 8 * mi + g, c = 8 * (j0 + x) + 2 * q + e;
+          sW[m * SLDW + c] = c2[x][e];
+          Rr[m + (size_t)c * b] = sR[c * SLDC + m] - c2[x][e];
+        }
+      }
+    }
+    __syncthreads();
+    TF_LU_T(26);
+    // ---- A -= V W2 on the resident accumulators (V operand one k-step ahead)
+    {
+      double an[MI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) an[i] = -Vs[(r0 + 8 * i + g) + (size_t)q * b];
+      for (int ks = 0; ks < nw / 4; ++ks) {
+        double a[MI], bq[SNJ];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) a[i] = an[i];
+        if (ks + 1 < nw / 4) {
+#pragma unroll
+          for (int i = 0; i < MI; ++i) an[i] = -Vs[(r0 + 8 * i + g) + (size_t)(4 * (ks + 1) + q) * b];
+        }
+#pragma unroll
+        for (int j = 0; j < SNJ; ++j) bq[j] = sW[(4 * ks + q) * SLDW + 8 * j + g];
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < SNJ; ++j) dmma(acc[i][j], a[i], bq[j]);
+      }
+    }
+    TF_LU_T(27);
+    __syncthreads();  // sW (W2) / sT / sR are rewritten by the next block
+    if (c0 + ib < b) mirror();
+    TF_LU_T(28);
+  }
+  slab_store<MI>(acc, A, b);
 }
 
 // SSRFB item: 32 columns of [R_kj; A_ij] <- Q_ik^T [R_kj; A_ij], blocks s = 0..t-1.

@@ -145,13 +145,13 @@ int main(int argc, char** argv) {
 #endif
 #ifdef TF_PROF_LU
   {
-    long long z[24] = {0}, h[24];
+    long long z[32] = {0}, h[32];
     cudaMemcpyToSymbol(g_lu_prof, z, sizeof(z));
     kb_kernel<<<grid, TF_THREADS, SMEM_DOUBLES * 8>>>(kind, b, ib, tiles, aux, ipiv, scratch, scr, reps, shared_ab);
     CK(cudaDeviceSynchronize());
     cudaMemcpyFromSymbol(h, g_lu_prof, sizeof(h));
     printf("lu phases us/task:");
-    for (int i = 0; i < 24; ++i) if (h[i]) printf(" [%d] %.1f", i, h[i] / 1.92e3 / grid / reps);
+    for (int i = 0; i < 32; ++i) if (h[i]) printf(" [%d] %.1f", i, h[i] / 1.92e3 / grid / reps);
     printf("\n");
   }
 #endif

@@ -215,16 +215,17 @@ __device__ __forceinline__ void lu_ts_apply_t(double (&acc)[MI][SNJ][2], double*
   double an[MI];
   if (!NPRE) {
 #pragma unroll
-    for (int i = 0; i < MI; ++i) an[i] = -Lc[(r0 + 8 * i + g) + (size_t)q * b];
+    for (int i = 0; i < MI; ++i) an[i] = Lc[(r0 + 8 * i + g) + (size_t)q * b];
   }
 #pragma unroll
   for (int ks = 0; ks < IB / 4; ++ks) {
     double a[MI], bq[SNJ];
+    // (the sign folds into the DMMA operand modifier; no DADD on the shared FP64 pipe)
 #pragma unroll
-    for (int i = 0; i < MI; ++i) a[i] = NPRE ? la[NPRE ? ks : 0][i] : an[i];
+    for (int i = 0; i < MI; ++i) a[i] = NPRE ? la[NPRE ? ks : 0][i] : -an[i];
     if (!NPRE && ks + 1 < IB / 4) {
 #pragma unroll
-      for (int i = 0; i < MI; ++i) an[i] = -Lc[(r0 + 8 * i + g) + (size_t)(4 * (ks + 1) + q) * b];
+      for (int i = 0; i < MI; ++i) an[i] = Lc[(r0 + 8 * i + g) + (size_t)(4 * (ks + 1) + q) * b];
     }
 #pragma unroll
     for (int j = 0; j < SNJ; ++j) bq[j] = sU[(4 * ks + q) * LU_LDW + 8 * j + g];

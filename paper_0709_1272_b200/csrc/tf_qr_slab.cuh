@@ -354,23 +354,25 @@ __device__ inline void ssrfb_mirror(const Ctx& cx, const double* V, const double
     TF_LU_T(26);
     // ---- A -= V W2 on the resident accumulators (V operand one k-step ahead)
     {
+      // (the sign is applied at the DMMA, where it folds into the operand modifier; negating
+      // at load time costs a DADD on the FP64 pipe the DMMAs share)
       double an[MI];
 #pragma unroll
-      for (int i = 0; i < MI; ++i) an[i] = -Vs[(r0 + 8 * i + g) + (size_t)q * b];
+      for (int i = 0; i < MI; ++i) an[i] = Vs[(r0 + 8 * i + g) + (size_t)q * b];
       for (int ks = 0; ks < nw / 4; ++ks) {
         double a[MI], bq[SNJ];
 #pragma unroll
         for (int i = 0; i < MI; ++i) a[i] = an[i];
         if (ks + 1 < nw / 4) {
 #pragma unroll
-          for (int i = 0; i < MI; ++i) an[i] = -Vs[(r0 + 8 * i + g) + (size_t)(4 * (ks + 1) + q) * b];
+          for (int i = 0; i < MI; ++i) an[i] = Vs[(r0 + 8 * i + g) + (size_t)(4 * (ks + 1) + q) * b];
         }
 #pragma unroll
         for (int j = 0; j < SNJ; ++j) bq[j] = sW[(4 * ks + q) * SLDW + 8 * j + g];
 #pragma unroll
         for (int i = 0; i < MI; ++i)
 #pragma unroll
-          for (int j = 0; j < SNJ; ++j) dmma(acc[i][j], a[i], bq[j]);
+          for (int j = 0; j < SNJ; ++j) dmma(acc[i][j], -a[i], bq[j]);
       }
     }
     TF_LU_T(27);

@@ -405,28 +405,12 @@ __device__ inline void gessm_reg(const Ctx& cx, const double* LX, const int* ipi
   slab_store<MI>(acc, C, b);
 }
 
-// LU panel of one 32-column slab held as P (smem, b x 32, column-major, ld ldp) on entry and
-// exit.  Row-per-thread during the factorization: thread t < b keeps row t of the slab (32
-// doubles) in registers, so the pivot search of a column is a reduction over threads and
-// the rank-1 update is 31 - jj FMAs per thread with the pivot row broadcast from smem.
-//   TS (TSTRF, PAPER.md:495-513): pairwise pivoting of column jj between the top row jj of
-//       UL (32 x 33: U of the slab's diagonal block above the diagonal, the L-strip block
-//       below it, footnote PAPER.md:542-544) and all b rows of P; the top row wins ties
-//       (first maximum in stacked order, Z11).  A swap exchanges the whole 32-entry row.
-//       pivots: b + r + 1 (row r swapped in) or cs + jj + 1 (kept), Z13.
-//   !TS (GETRF, PAPER.md:477-486): partial pivoting over tile rows >= cs + jj of P (first
-//       maximum), rows swapped over the slab's 32 columns (the caller applies them to the
-//       other columns, Z12); pivots cs-relative rows + 1 in [1, b].
-// Column jj, ONE CTA barrier: every warp reduces its 32 rows to (max |x|, first row) with
-// three redux.sync (max of the high word, max of the low word among those, min row among
-// those: |x| >= 0 orders like its bit pattern) and its winning lane publishes the whole
-// candidate row (GETRF also publishes row cs + jj) into parity-double-buffered smem;
-// after the barrier every warp merges the 16 warp candidates the same way, so all threads
-// know the pivot row and read its values from the winner's published copy.  The swap, the
-// division by the pivot (division, as the oracle) and the update follow without another
-// barrier.  Returns the first zero-pivot local column or -1.
+__device__ __forceinline__ void bar_named(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 __device__ __forceinline__ void warp_first_max(double v, int idx, double& bv, int& bi) {
-  // v >= 0 (fabs), idx = row (INT_MAX: no candidate).  Largest v, then smallest idx.
+  // v >= 0 (fabs), idx = key (INT_MAX: no candidate).  Largest v, then smallest idx.
   const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
   const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
   const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
@@ -434,101 +418,145 @@ __device__ __forceinline__ void warp_first_max(double v, int idx, double& bv, in
   bv = __hiloint2double((int)mhi, (int)mlo);
 }
 
+constexpr int ULD = 34;  // row stride of the TSTRF top block UL (16-byte aligned rows)
+
+// LU panel of one 32-column slab held as P (smem, b x 32, column-major, ld ldp) on entry and
+// exit.  Row-per-thread: thread t < b keeps row t of the slab (32 doubles) in registers, so
+// the pivot search of a column is a reduction over threads and the rank-1 update is
+// 31 - jj FMAs per thread with the pivot row broadcast from smem.
+//   TS (TSTRF, PAPER.md:495-513): pairwise pivoting of column jj between the top row jj of
+//       UL (32 x ULD: U of the slab's diagonal block above the diagonal, the L-strip block
+//       below it, footnote PAPER.md:542-544) and all b rows of P; the top row wins ties
+//       (first maximum in stacked order, Z11).  A swap exchanges the whole 32-entry row.
+//       pivots: b + r + 1 (row r swapped in) or cs + jj + 1 (kept), Z13.
+//   !TS (GETRF, PAPER.md:477-486): partial pivoting over tile rows >= cs + jj of P (first
+//       maximum), rows interchanged over the slab's 32 columns (the caller applies them to
+//       the other columns, Z12); pivots cs-relative rows + 1 in [1, b].  The interchanges
+//       are applied lazily: thread t tracks the row position `pos` its registers hold (an
+//       interchange swaps two positions, no data moves), candidates and ties are decided on
+//       positions (first maximum = smallest position), and rows land at their final
+//       positions when the panel is written back.
+// Column jj, TWO barriers over the warps that own rows (named barrier; the other warps
+// skip the panel): (A) every warp publishes its candidate (max |x|, smallest position
+// among the maxima, and that row's reciprocal, formed while the reductions run) with one
+// lane's stores; after A every warp merges the candidates the same way, so all threads
+// know the pivot row, and only the pivot row's thread publishes its columns jj..31;
+// (B) then division (x r with the division's own correction, = x / upiv bitwise), the
+// update of column jj + 1 first, column jj + 1's warp candidates, and the rest of the
+// rank-1 update while the reductions run.  (Measured: a barrier after s one-lane 128-bit
+// shared stores per warp costs ~5.5 cycles per store instruction in the CTA, so the
+// round-1 design — every warp's candidate publishing its whole row and one barrier —
+// spent ~0.8-1.4k cycles per column on the store drain; tools/lat_stsbar.cu.)
+// Returns the first zero-pivot local column or -1.
 template <int MI, bool TS>
 __device__ inline int lu_panel(double* P, int ldp, int cs, int b, double* UL, int* piv, double* sm2, int nopiv) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwa = (b + 31) >> 5;                         // warps that own rows
   const bool own = tid < b;
-  double* cval = sm2;                                    // 2 x 16 warp maxima
-  int* cidx = reinterpret_cast<int*>(sm2 + 32);          // 2 x 16 warp argmax rows
-  double* crow = sm2 + 64;                               // 2 x 16 x 32 candidate rows
-  double* trow = crow + 2 * 16 * 32;                     // 2 x 32: GETRF row cs + jj (pre-swap)
+  double2* sv = reinterpret_cast<double2*>(sm2);         // [2][16] {max |x|, reciprocal}
+  int* sk = reinterpret_cast<int*>(sm2 + 64);            // [2][16] key = position << 4 | warp
+  double* urow = sm2 + 80;                               // [2][32] the pivot row
+  int* fzp = reinterpret_cast<int*>(sm2 + 144);
   double x[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) x[c] = own ? P[tid + (size_t)c * ldp] : 0.0;
+  int pos = tid;
   int first_zero = -1;
-  TF_LU_T0();
-#pragma unroll
-  for (int jj = 0; jj < 32; ++jj) {
-    const int par = jj & 1;
-    const int cg = cs + jj;
-    // (TSTRF) the top candidate is read before the barrier: the winner rewrites UL row jj
-    // after it, while slower warps may still be comparing
-    const double top = TS ? fabs(UL[jj * 33 + jj]) : 0.0;
-    if (warp < nwa) {
-      // GENP (nopiv): GETRF's only candidate is row cg; TSTRF keeps the top row
-      const bool cand = own && (TS ? !nopiv : (nopiv ? tid == cg : tid >= cg));
-      double wv;
-      int wi;
-      warp_first_max(cand ? fabs(x[jj]) : 0.0, cand ? tid : INT_MAX, wv, wi);
-      if (lane == 0) {
-        cval[par * 16 + warp] = wv;
-        cidx[par * 16 + warp] = wi;
-      }
-      if (tid == wi) {
-        double2* d = reinterpret_cast<double2*>(crow + (par * 16 + warp) * 32);
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) d[c >> 1] = make_double2(x[c], x[c + 1]);
-      }
-      if (!TS && tid == cg) {
-        double2* d = reinterpret_cast<double2*>(trow + par * 32);
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) d[c >> 1] = make_double2(x[c], x[c + 1]);
-      }
+  // the warp's candidate for column jj -> slot (par, warp); GENP (nopiv): GETRF's only
+  // candidate is position cs + jj, TSTRF keeps the top row
+  auto candidate = [&](int jj, int par) {
+    const bool cand = own && (TS ? !nopiv : (nopiv ? pos == cs + jj : pos >= cs + jj));
+    const int key = cand ? (pos << 4 | warp) : INT_MAX;
+    const double rr = rcp_newton(x[jj]);
+    double wv;
+    int wk;
+    warp_first_max(cand ? fabs(x[jj]) : 0.0, key, wv, wk);
+    if (wk == INT_MAX ? lane == 0 : key == wk) {
+      sv[par * 16 + warp] = make_double2(wv, rr);
+      sk[par * 16 + warp] = wk;
     }
-    TF_LU_T(12);
-    __syncthreads();
-    TF_LU_T(13);
-    if (warp >= nwa) continue;
-    // the winner over the warp candidates (lane w holds warp w's), first maximum
-    double bv;
-    int bi;
-    warp_first_max(lane < nwa ? cval[par * 16 + lane] : 0.0, lane < nwa ? cidx[par * 16 + lane] : INT_MAX, bv, bi);
-    int pr = bi;                                         // winning row (GETRF: row >= cg exists)
-    if (TS && !(bv > top)) pr = -1;                      // the top row wins ties
-    const double* u = (!TS || pr >= 0) ? crow + (par * 16 + (pr >> 5)) * 32 : UL + jj * 33;  // the pivot row
-    if (TS) {
-      if (pr >= 0 && tid == pr) {  // row pr <-> top row jj (the whole 32-entry row)
+  };
+  TF_LU_T0();
+  if (warp < nwa) {
+    candidate(0, 0);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const double t = UL[jj * 33 + c];
-          UL[jj * 33 + c] = x[c];
-          x[c] = t;
+    for (int jj = 0; jj < 32; ++jj) {
+      const int par = jj & 1;
+      const int cg = cs + jj;
+      // (TSTRF) the top candidate and its reciprocal, before A (the winner rewrites UL row
+      // jj after B; nothing else writes it)
+      const double top = TS ? UL[jj * ULD + jj] : 0.0;
+      const double rtop = TS ? rcp_newton(top) : 0.0;
+      TF_LU_T(12);
+      bar_named(1, nwa * 32);
+      TF_LU_T(13);
+      double2 v = make_double2(0.0, 0.0);
+      int k = INT_MAX;
+      if (lane < nwa) {
+        v = sv[par * 16 + lane];
+        k = sk[par * 16 + lane];
+      }
+      double bv;
+      int kmin;
+      warp_first_max(v.x, k, bv, kmin);
+      double r = __shfl_sync(0xffffffffu, v.y, kmin & 15);
+      int pr = kmin == INT_MAX ? -1 : kmin >> 4;         // GETRF: a candidate always exists
+      if (TS && !(bv > fabs(top))) {                     // the top row wins ties
+        pr = -1;
+        r = rtop;
+      }
+      const bool win = TS ? (pr >= 0 && tid == pr) : (pos == pr);
+      if (win) {
+#pragma unroll
+        for (int c = jj & ~1; c < 32; c += 2)
+          *reinterpret_cast<double2*>(urow + par * 32 + c) = make_double2(x[c], x[c + 1]);
+      }
+      TF_LU_T(14);
+      bar_named(1, nwa * 32);
+      const double* u = (TS && pr < 0) ? UL + jj * ULD : urow + par * 32;
+      if (tid == 0) piv[jj] = TS ? (pr >= 0 ? b + pr + 1 : cg + 1) : pr + 1;
+      if (TS) {
+        if (win) {  // row pr <-> top row jj (the whole 32-entry row)
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(UL + jj * ULD + c);
+            *reinterpret_cast<double2*>(UL + jj * ULD + c) = make_double2(x[c], x[c + 1]);
+            x[c] = t.x;
+            x[c + 1] = t.y;
+          }
+        }
+      } else if (win) {
+        pos = cg;
+      } else if (pos == cg) {
+        pos = pr;
+      }
+      const double upiv = u[jj];
+      const bool elim = own && (TS || pos > cg) && upiv != 0.0;
+      double l = 0.0;
+      if (elim) {
+        l = div_rcp(x[jj], upiv, r);
+        x[jj] = l;
+        if (jj < 31) x[jj + 1] = fma(-l, u[jj + 1], x[jj + 1]);
+      }
+      if (upiv == 0.0 && first_zero < 0) first_zero = jj;
+      if (jj < 31) {
+        candidate(jj + 1, par ^ 1);
+        if (elim) {
+#pragma unroll
+          for (int c = jj + 2; c < 32; ++c) x[c] = fma(-l, u[c], x[c]);
         }
       }
-    } else if (pr != cg) {
-      if (tid == cg) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) x[c] = u[c];
-      } else if (tid == pr) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) x[c] = trow[par * 32 + c];
-      }
+      TF_LU_T(15);
     }
-    if (tid == 0) piv[jj] = TS ? (pr >= 0 ? b + pr + 1 : cg + 1) : pr + 1;
-    TF_LU_T(14);
-    const double upiv = u[jj];
-    if (upiv != 0.0) {
-      if (own && (TS || tid > cg)) {
-        const double l = x[jj] / upiv;
-        x[jj] = l;
-#pragma unroll
-        for (int c = jj + 1; c < 32; ++c) x[c] = fma(-l, u[c], x[c]);
-      }
-    } else if (first_zero < 0) {
-      first_zero = jj;
-    }
-    TF_LU_T(15);
   }
   if (own) {
 #pragma unroll
-    for (int c = 0; c < 32; ++c) P[tid + (size_t)c * ldp] = x[c];
+    for (int c = 0; c < 32; ++c) P[pos + (size_t)c * ldp] = x[c];
   }
   // warps without rows skipped the pivot tests: every thread takes thread 0's first_zero
-  int* fz = cidx + 32;
-  if (tid == 0) *fz = first_zero;
+  if (tid == 0) *fzp = first_zero;
   __syncthreads();
-  first_zero = *fz;
+  first_zero = *fzp;
   __syncthreads();
   return first_zero;
 }
@@ -576,7 +604,7 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
     TF_LU_T(8);
     double* P = sm;
     double* UL = P + 32 * ldp;
-    double* sm2 = UL + 32 * 33;
+    double* sm2 = UL + 32 * ULD;
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -585,7 +613,7 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
         for (int e = 0; e < 2; ++e) P[(r0 + 8 * i + g) + (size_t)(8 * j + 2 * q + e) * ldp] = acc[i][j][e];
     for (int e = tid; e < 32 * 32; e += TF_THREADS) {
       const int rr = e % 32, cc = e / 32;
-      UL[rr * 33 + cc] = (rr <= cc) ? ldg_cg(U + (cs + rr) + (size_t)(cs + cc) * b) : 0.0;
+      UL[rr * ULD + cc] = (rr <= cc) ? ldg_cg(U + (cs + rr) + (size_t)(cs + cc) * b) : 0.0;
     }
     __syncthreads();
     TF_LU_T(9);
@@ -598,8 +626,8 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
     }
     for (int e = tid; e < 32 * 32; e += TF_THREADS) {
       const int rr = e % 32, cc = e / 32;
-      if (rr <= cc) U[(cs + rr) + (size_t)(cs + cc) * b] = UL[rr * 33 + cc];
-      Ls[(size_t)(cs + cc) * ib + off + rr] = rr > cc ? UL[rr * 33 + cc] : 0.0;
+      if (rr <= cc) U[(cs + rr) + (size_t)(cs + cc) * b] = UL[rr * ULD + cc];
+      Ls[(size_t)(cs + cc) * ib + off + rr] = rr > cc ? UL[rr * ULD + cc] : 0.0;
       if (ib == 2 * NSR) Ls[(size_t)(cs + cc) * ib + (NSR - off) + rr] = 0.0;  // the other half's rows
     }
     __syncthreads();

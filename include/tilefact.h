@@ -141,6 +141,13 @@ int tile_factor_host(int kind, int64_t n, int64_t b, int64_t ib, double* hA, dou
  * couple-update); 1 = kind ranks plus a lookahead boost for updates of tile column k+1
  * (default).  Applies to subsequent calls on this process. */
 void tile_set_policy(int policy);
+
+/* Task-graph granularity for QR / LU on one GPU (b in {128, 256, 512}, ib in {32, 64}):
+ * 1 = slab-level graph (panel tasks per 32-column slab, next-column updates per slab
+ * item; the default), 0 = the paper's tile-level graph, -1 = default
+ * (environment TF_FINE=0 selects tile-level).  Results are bitwise identical; applies to
+ * subsequent calls on this process. */
+void tile_set_slab_dag(int on);
 /* Enable (cap > 0) / disable (0) the device trace: one record per work item
  * {task, item, sm, start_ns, end_ns}.  tile_trace_fetch copies the last call's records
  * (synchronizes that stream) into rec (5 int64 per record) and returns the count. */
@@ -158,6 +165,17 @@ void tile_set_ctas(int ctas);
 int64_t tile_dag_export(int alg, int64_t p, int policy, int32_t* kind, int32_t* k, int32_t* i,
                         int32_t* j, int32_t* level, int64_t cap, int64_t* succ_off, int32_t* succ,
                         int64_t succ_cap, int64_t* nedges);
+
+/* Slab-level task graph of QR (alg 1) / LU (alg 2) for tile size b, inner block ib (the
+ * graph tile_qr / tile_lu run on one GPU when b is in {128, 256, 512} and ib in {32, 64};
+ * DESIGN.md §6).  As tile_dag_export plus slab[t]: for the panel kinds 25 GEQRT-slab,
+ * 26 TSQRT-slab, 27 GETRF-slab, 28 TSTRF-slab the 32-column slab the task factors; for
+ * kinds 5 / 7 / 9 / 11 with one item, the slab item it runs (whole update tasks: 0).
+ * Returns the task count, or -1 when (alg, b, ib) has no slab-level graph. */
+int64_t tile_dag_export_slab(int alg, int64_t p, int64_t b, int64_t ib, int policy, int32_t* kind,
+                             int32_t* k, int32_t* i, int32_t* j, int32_t* slab, int32_t* level,
+                             int64_t cap, int64_t* succ_off, int32_t* succ, int64_t succ_cap,
+                             int64_t* nedges);
 
 /* Run one tile kernel on the given device tiles (kernel-level parity tests).
  * kind as in tile_dag_export; t0..t2 per kind:

@@ -332,19 +332,30 @@ __device__ inline void run_item(const Prob& P, const Sched& S, const Dist& D, co
     case 2: syrk_item(cx, a.T(i, k), a.T(i, i), sub, sm); break;
     case 3: gemm_item(cx, a.T(i, k), a.T(j, k), a.T(i, j), sub, sm); break;
     case 4: geqrt_item(cx, a.T(k, k), a.STRIP(k, k), a.VX(k), sm); break;
-    case 5: larfb_item(cx, a.VX(k), a.STRIP(k, k), a.T(k, j), sub, sm); break;
+    case 5: larfb_item(cx, a.VX(k), a.STRIP(k, k), a.T(k, j), sub + d.pad, sm); break;
     case 6: tsqrt_item(cx, a.T(k, k), a.T(i, k), a.STRIP(i, k), sm); break;
-    case 7: ssrfb_item(cx, a.T(i, k), a.STRIP(i, k), a.T(k, j), a.T(i, j), sub, sm); break;
+    case 7: ssrfb_item(cx, a.T(i, k), a.STRIP(i, k), a.T(k, j), a.T(i, j), sub + d.pad, sm); break;
     case 8: {
       const int f = getrf_item(cx, a.T(k, k), a.PIV(k, k), a.VX(k), sm);
       if (f >= 0 && threadIdx.x == 0) atomicMin(cx.info, k * P.b + f + 1);
     } break;
-    case 9: gessm_item(cx, a.VX(k), a.PIV(k, k), a.T(k, j), sub, sm); break;
+    case 9: gessm_item(cx, a.VX(k), a.PIV(k, k), a.T(k, j), sub + d.pad, sm); break;
     case 10: {
       const int f = tstrf_item(cx, a.T(k, k), a.T(i, k), a.STRIP(i, k), a.PIV(i, k), sm);
       if (f >= 0 && threadIdx.x == 0) atomicMin(cx.info, k * P.b + f + 1);
     } break;
-    case 11: ssssm_item(cx, a.T(i, k), a.STRIP(i, k), a.PIV(i, k), a.T(k, j), a.T(i, j), sub, sm); break;
+    case 11: ssssm_item(cx, a.T(i, k), a.STRIP(i, k), a.PIV(i, k), a.T(k, j), a.T(i, j), sub + d.pad, sm); break;
+    // slab-level DAG panel tasks (d.pad = slab)
+    case K_GEQRT_S: geqrt_slab_item(cx, a.T(k, k), a.STRIP(k, k), a.VX(k), d.pad, sm); break;
+    case K_TSQRT_S: tsqrt_slab_item(cx, a.T(k, k), a.T(i, k), a.STRIP(i, k), d.pad, sm); break;
+    case K_GETRF_S: {
+      const int f = getrf_slab_item(cx, a.T(k, k), a.PIV(k, k), a.VX(k), d.pad, sm);
+      if (f >= 0 && threadIdx.x == 0) atomicMin(cx.info, k * P.b + f + 1);
+    } break;
+    case K_TSTRF_S: {
+      const int f = tstrf_slab_item(cx, a.T(k, k), a.T(i, k), a.STRIP(i, k), a.PIV(i, k), d.pad, sm);
+      if (f >= 0 && threadIdx.x == 0) atomicMin(cx.info, k * P.b + f + 1);
+    } break;
     // solve / apply tasks (tf_solve.cuh); d.j = the right-hand-side tile column c
     case K_UNITL: unitl_item(cx, a.T(k, k), a.VX(k)); break;
     case K_XGESSM: gessm_item(cx, a.VX(k), a.PIV(k, k), a.X(k, j), sub, sm); break;

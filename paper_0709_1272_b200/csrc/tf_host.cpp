@@ -52,6 +52,7 @@ void set_err(const char* fmt, ...) {
   } while (0)
 
 int g_policy = 1;
+int g_slab_dag = -1;  // tile_set_slab_dag: -1 = default (TF_FINE env, on), 0 = tile-level, 1 = slab-level
 int64_t g_trace_cap = 0;
 int g_ctas = 0;
 std::recursive_mutex g_mu;
@@ -149,6 +150,87 @@ void global_tasks(int alg, int p, int b, int ib, int policy, std::vector<TaskD>&
         P(i == k + 1 ? get(R, k, k, j) : get(U, k, i - 1, j));
         if (k > 0) P(get(U, k - 1, i, j));
       }
+    }
+  }
+}
+
+// Slab-level DAG of Algorithms 2-3 (QR / LU on the register-slab kernels, single GPU).
+// The panel tasks become one task per 32-column slab s (GEQRT / GETRF: FS(k,s); TSQRT /
+// TSTRF: CS(k,i,s)), and the update tasks of the next panel column, LARFB / GESSM (k,k+1)
+// and SSRFB / SSSSM (k,i,k+1), one task per slab item.  Every slab of a panel task reads
+// only global results of the slabs before it (left-looking) and touches the diagonal tile
+// only in its own columns (TSQRT / TSTRF: the upper part of R_kk / U_kk; GETRF's later
+// interchanges move only rows below the slab's diagonal block), so
+//   FS(k,s)      <- FS(k,s-1), U(k-1,k,k) slab s
+//   CS(k,i,s)    <- CS(k,i,s-1), [i == k+1 ? FS(k,s) : CS(k,i-1,s)], U(k-1,i,k) slab s
+//   R(k,j)[s]    <- FS(k,last), U(k-1,k,j)
+//   U(k,i,j)[s]  <- CS(k,i,last), [i == k+1 ? R(k,j)[s] : U(k,i-1,j)[s]], U(k-1,i,j)
+// (slab s where the producer is split, the whole task otherwise).  Consecutive TSQRT /
+// TSTRF of a tile column then overlap slab by slab, and the next panel starts on its
+// first slab while the lookahead updates of its later slabs run; each tile sees the same
+// operations in the same order as in the tile-level DAG (results are bitwise identical).
+void global_tasks_fine(int alg, int p, int b, int ib, int policy, std::vector<TaskD>& tasks,
+                       std::vector<std::vector<int>>& preds, int qc = -1) {
+  if (qc < 0) qc = p;
+  const int S = b / NSR;
+  const int F = alg == 1 ? 4 : 8, R = F + 1, C = F + 2, U = F + 3;
+  const int FS = alg == 1 ? K_GEQRT_S : K_GETRF_S, CS = alg == 1 ? K_TSQRT_S : K_TSTRF_S;
+  std::unordered_map<uint64_t, int> id;
+  tasks.clear();
+  // split (per-slab) tasks: key kind | 32, j' = j * 64 + s
+  auto key = [&](int kind, int k, int i, int j, int s) {
+    return s < 0 ? key4(kind, k, i, j) : key4(kind | 32, k, i, j * 64 + s);
+  };
+  auto add = [&](int kind, int k, int i, int j, int s, int nit) {
+    TaskD d{kind, k, i, j, nit, 0, level_of(coarse_kind(kind), k, j, policy), s < 0 ? 0 : s};
+    id[key(kind, k, i, j, s)] = (int)tasks.size();
+    tasks.push_back(d);
+  };
+  const int nit = items_of(U, b, ib);  // slab items of an update task (= S)
+  const int kk = p < qc ? p : qc;
+  for (int k = 0; k < kk; ++k) {
+    for (int s = 0; s < S; ++s) add(FS, k, k, k, s, 1);
+    for (int j = k + 1; j < qc; ++j) {
+      if (j == k + 1) for (int s = 0; s < nit; ++s) add(R, k, k, j, s, 1);
+      else add(R, k, k, j, -1, nit);
+    }
+    for (int i = k + 1; i < p; ++i) {
+      for (int s = 0; s < S; ++s) add(CS, k, i, k, s, 1);
+      for (int j = k + 1; j < qc; ++j) {
+        if (j == k + 1) for (int s = 0; s < nit; ++s) add(U, k, i, j, s, 1);
+        else add(U, k, i, j, -1, nit);
+      }
+    }
+  }
+  auto get = [&](int kind, int k, int i, int j, int s) -> int {
+    auto it = id.find(key(kind, k, i, j, s));
+    return it == id.end() ? -1 : it->second;
+  };
+  // update task (k,i,j) or its slab s (split iff j == k + 1); s = -1: the whole task
+  auto upd = [&](int kind, int k, int i, int j, int s) { return get(kind, k, i, j, j == k + 1 ? s : -1); };
+  const int nt = (int)tasks.size();
+  preds.assign(nt, {});
+  for (int t = 0; t < nt; ++t) {
+    const TaskD& d = tasks[t];
+    auto& pr = preds[t];
+    auto P = [&](int x) { if (x >= 0 && std::find(pr.begin(), pr.end(), x) == pr.end()) pr.push_back(x); };
+    const int k = d.k, i = d.i, j = d.j, s = d.pad;
+    const bool split = d.nitems == 1 && (d.kind == R || d.kind == U);
+    if (d.kind == FS) {
+      if (s > 0) P(get(FS, k, k, k, s - 1));
+      if (k > 0) P(upd(U, k - 1, k, k, s));
+    } else if (d.kind == CS) {
+      if (s > 0) P(get(CS, k, i, k, s - 1));
+      P(i == k + 1 ? get(FS, k, k, k, s) : get(CS, k, i - 1, k, s));
+      if (k > 0) P(upd(U, k - 1, i, k, s));
+    } else if (d.kind == R) {
+      P(get(FS, k, k, k, S - 1));
+      if (k > 0) P(upd(U, k - 1, k, j, split ? s : -1));
+    } else if (d.kind == U) {
+      P(get(CS, k, i, k, S - 1));
+      const int sx = split ? s : -1;  // (j == k + 1 exactly when split)
+      P(i == k + 1 ? get(R, k, k, j, sx) : get(U, k, i - 1, j, sx));
+      if (k > 0) P(get(U, k - 1, i, j, -1));  // split iff j == k; here j >= k + 1: the whole task
     }
   }
 }
@@ -267,7 +349,7 @@ void add_copy_tasks(int alg, int p, int b, int ib, std::vector<TaskD>& tasks, st
   preds.resize(tasks.size());
   for (int t = 0; t < nt; ++t) {
     const TaskD& d = tasks[t];
-    const int k = d.k, i = d.i, j = d.j;
+    const int k = d.k, i = d.i, j = d.j, kind = coarse_kind(d.kind);
     int rd[3][2], wr[2][2], nr = 0, nw = 0;
     auto R = [&](int r, int c) { rd[nr][0] = r; rd[nr][1] = c; ++nr; };
     auto W = [&](int r, int c) { wr[nw][0] = r; wr[nw][1] = c; ++nw; };
@@ -280,9 +362,9 @@ void add_copy_tasks(int alg, int p, int b, int ib, std::vector<TaskD>& tasks, st
       }
     } else {
       const int F = alg == 1 ? 4 : 8;
-      if (d.kind == F) W(k, k);
-      else if (d.kind == F + 1) { R(k, k); W(k, j); }
-      else if (d.kind == F + 2) { W(k, k); W(i, k); }
+      if (kind == F) W(k, k);
+      else if (kind == F + 1) { R(k, k); W(k, j); }
+      else if (kind == F + 2) { W(k, k); W(i, k); }
       else { R(i, k); W(k, j); W(i, j); }
     }
     for (int x = 0; x < nr + nw; ++x) {
@@ -302,10 +384,22 @@ void add_copy_tasks(int alg, int p, int b, int ib, std::vector<TaskD>& tasks, st
     }
 }
 
-void build_dag(HostDag& G, int alg, int p, int b, int ib, int policy, int q = 0, int qc = -1, int e2e = 0) {
+// The slab-level DAG is used for QR / LU on the register-slab kernels (TF_FINE=0 selects the
+// tile-level DAG, for comparison).
+bool fine_dag(int alg, int b, int ib) {
+  static const int env = getenv("TF_FINE") ? atoi(getenv("TF_FINE")) : 1;
+  const int on = g_slab_dag >= 0 ? g_slab_dag : env;
+  return on != 0 && (alg == 1 || alg == 2) && ssrfb_reg_ok(b, ib);
+}
+
+// fine: -1 = fine_dag()'s choice, 0 = tile-level, 1 = slab-level where eligible.
+void build_dag(HostDag& G, int alg, int p, int b, int ib, int policy, int q = 0, int qc = -1, int e2e = 0,
+               int fine = -1) {
   G.alg = alg; G.p = p; G.b = b; G.policy = policy;
   std::vector<std::vector<int>> preds;
   if (alg >= ALG_GETRS) solve_tasks(alg, p, b, ib, q, policy, G.tasks, preds);
+  else if (fine < 0 ? fine_dag(alg, b, ib) : (fine > 0 && (alg == 1 || alg == 2) && ssrfb_reg_ok(b, ib)))
+    global_tasks_fine(alg, p, b, ib, policy, G.tasks, preds, qc);
   else global_tasks(alg, p, b, ib, policy, G.tasks, preds, qc);
   if (e2e) add_copy_tasks(alg, p, b, ib, G.tasks, preds);
   finalize_dag(G, preds);
@@ -468,7 +562,7 @@ void free_dag(DevDag& D) {
 }
 
 int get_dag(int dev, int alg, int p, int b, int ib, DevDag** out, int q = 0, int qc = -1, int e2e = 0) {
-  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy, q, qc, e2e);
+  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy * 4 + (fine_dag(alg, b, ib) ? 2 : 0), q, qc, e2e);
   auto it = g_dags.find(key);
   if (it != g_dags.end()) { *out = &it->second; return 0; }
   DevDag D;
@@ -1120,6 +1214,7 @@ int tile_factor_host(int kind, int64_t n, int64_t b, int64_t ib, double* hA, dou
 }
 
 void tile_set_policy(int policy) { g_policy = (policy == 0) ? 0 : 1; }
+void tile_set_slab_dag(int on) { g_slab_dag = on < 0 ? -1 : (on ? 1 : 0); }
 void tile_set_trace(int64_t cap) { g_trace_cap = cap > 0 ? cap : 0; }
 void tile_set_ctas(int ctas) { g_ctas = ctas > 0 ? ctas : 0; }
 
@@ -1140,13 +1235,37 @@ int64_t tile_dag_export(int alg, int64_t p, int policy, int32_t* kind, int32_t* 
                         int64_t* nedges) {
   if (alg < 0 || alg > ALG_LUN || p <= 0) return -1;
   HostDag G;
-  build_dag(G, alg, (int)p, 128, 32, policy, alg >= ALG_GETRS ? 1 : 0);
+  build_dag(G, alg, (int)p, 128, 32, policy, alg >= ALG_GETRS ? 1 : 0, -1, 0, /*fine=*/0);
   const int64_t nt = (int64_t)G.tasks.size();
   for (int64_t t = 0; t < nt && t < cap; ++t) {
     if (kind) kind[t] = G.tasks[t].kind;
     if (k) k[t] = G.tasks[t].k;
     if (i) i[t] = G.tasks[t].i;
     if (j) j[t] = G.tasks[t].j;
+    if (level) level[t] = G.tasks[t].level;
+  }
+  if (succ_off && cap >= nt)
+    for (int64_t t = 0; t <= nt; ++t) succ_off[t] = G.succ_off[t];
+  const int64_t ne = (int64_t)G.succ.size();
+  if (succ)
+    for (int64_t e = 0; e < ne && e < succ_cap; ++e) succ[e] = G.succ[e];
+  if (nedges) *nedges = ne;
+  return nt;
+}
+
+int64_t tile_dag_export_slab(int alg, int64_t p, int64_t b, int64_t ib, int policy, int32_t* kind, int32_t* k,
+                             int32_t* i, int32_t* j, int32_t* slab, int32_t* level, int64_t cap, int64_t* succ_off,
+                             int32_t* succ, int64_t succ_cap, int64_t* nedges) {
+  if ((alg != 1 && alg != 2) || p <= 0 || !ssrfb_reg_ok((int)b, (int)ib)) return -1;
+  HostDag G;
+  build_dag(G, alg, (int)p, (int)b, (int)ib, policy, 0, -1, 0, /*fine=*/1);
+  const int64_t nt = (int64_t)G.tasks.size();
+  for (int64_t t = 0; t < nt && t < cap; ++t) {
+    if (kind) kind[t] = G.tasks[t].kind;
+    if (k) k[t] = G.tasks[t].k;
+    if (i) i[t] = G.tasks[t].i;
+    if (j) j[t] = G.tasks[t].j;
+    if (slab) slab[t] = G.tasks[t].pad;
     if (level) level[t] = G.tasks[t].level;
   }
   if (succ_off && cap >= nt)

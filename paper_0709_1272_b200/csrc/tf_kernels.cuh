@@ -712,8 +712,9 @@ namespace tf {
     else fn<1>(__VA_ARGS__);                           \
   } while (0)
 
-TF_DEF_VARIANT(v_qr_slab, qr_slab, (Ctx cx, bool ts, double* A, double* R, double* Tst, double* VX),
-               (cx, ts, A, R, Tst, VX, dsm))
+TF_DEF_VARIANT(v_qr_slab, qr_slab,
+               (Ctx cx, bool ts, double* A, double* R, double* Tst, double* VX, int cb, int ce),
+               (cx, ts, A, R, Tst, VX, cb, ce, dsm))
 TF_DEF_VARIANT(v_larfb_reg, larfb_reg, (Ctx cx, const double* VX, const double* Tst, double* C, int item),
                (cx, VX, Tst, C, item, dsm))
 TF_DEF_VARIANT(v_ssrfb_reg, ssrfb_reg, (Ctx cx, const double* V, const double* Tst, double* R, double* A, int item),
@@ -729,8 +730,12 @@ TF_DEF_REF(v_ssrfb_ref, ssrfb_ref, (Ctx cx, const double* V, const double* Tst, 
 
 // GEQRT: A_kk -> V_kk, R_kk, T_kk; writes the unit-lower V copy VX.
 __device__ inline void geqrt_item(const Ctx& cx, double* A, double* Tst, double* VX, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_qr_slab, cx, false, A, nullptr, Tst, VX);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_qr_slab, cx, false, A, nullptr, Tst, VX, 0, cx.b);
   else v_geqrt_ref(cx, A, Tst, VX);
+}
+// GEQRT slab task of the slab-level DAG: 32-column slab s (register-slab path only).
+__device__ inline void geqrt_slab_item(const Ctx& cx, double* A, double* Tst, double* VX, int s, double* sm) {
+  TF_SLAB_DISPATCH(v_qr_slab, cx, false, A, nullptr, Tst, VX, s * NSR, (s + 1) * NSR);
 }
 // LARFB: slab `item` of C <- Q_kk^T C.
 __device__ inline void larfb_item(const Ctx& cx, const double* VX, const double* Tst, double* C, int item,
@@ -740,8 +745,12 @@ __device__ inline void larfb_item(const Ctx& cx, const double* VX, const double*
 }
 // TSQRT: QR of [R_kk; A_ik]; only the upper region of R_kk is touched.
 __device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* Tst, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_qr_slab, cx, true, A, R, Tst, nullptr);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_qr_slab, cx, true, A, R, Tst, nullptr, 0, cx.b);
   else v_tsqrt_ref(cx, R, A, Tst);
+}
+// TSQRT slab task of the slab-level DAG: 32-column slab s of [R_kk; A_ik].
+__device__ inline void tsqrt_slab_item(const Ctx& cx, double* R, double* A, double* Tst, int s, double* sm) {
+  TF_SLAB_DISPATCH(v_qr_slab, cx, true, A, R, Tst, nullptr, s * NSR, (s + 1) * NSR);
 }
 // SSRFB: slab `item` of [R_kj; A_ij] <- Q_ik^T [R_kj; A_ij].
 __device__ inline void ssrfb_item(const Ctx& cx, const double* V, const double* Tst, double* R, double* A,
@@ -1073,9 +1082,10 @@ TF_DEF_VARIANT(v_gessm_reg, gessm_reg, (Ctx cx, const double* LX, const int* ipi
 TF_DEF_VARIANT(v_ssssm_reg, ssssm_reg,
                (Ctx cx, const double* L, const double* Ls, const int* ipiv, double* U, double* A, int item),
                (cx, L, Ls, ipiv, U, A, item, dsm))
-TF_DEF_VARIANT_RET(v_getrf_slab, getrf_slab, (Ctx cx, double* A, int* ipiv, double* LX), (cx, A, ipiv, LX, dsm))
-TF_DEF_VARIANT_RET(v_tstrf_slab, tstrf_slab, (Ctx cx, double* U, double* A, double* Ls, int* ipiv),
-                   (cx, U, A, Ls, ipiv, dsm))
+TF_DEF_VARIANT_RET(v_getrf_slab, getrf_slab, (Ctx cx, double* A, int* ipiv, double* LX, int cb, int ce),
+                   (cx, A, ipiv, LX, cb, ce, dsm))
+TF_DEF_VARIANT_RET(v_tstrf_slab, tstrf_slab, (Ctx cx, double* U, double* A, double* Ls, int* ipiv, int cb, int ce),
+                   (cx, U, A, Ls, ipiv, cb, ce, dsm))
 TF_DEF_REF(v_gessm_ref, gessm_ref, (Ctx cx, const double* LX, const int* ipiv, double* C, int item),
            (cx, LX, ipiv, C, item, dsm))
 TF_DEF_REF(v_ssssm_ref, ssssm_ref,
@@ -1098,8 +1108,12 @@ __device__ inline void ssssm_item(const Ctx& cx, const double* L, const double* 
 // LU panel tasks: slab kernels for ib in {32, 64} (32-column slabs).
 #define TF_SLAB_RET(fn, ...) (cx.b == 512 ? fn<4>(__VA_ARGS__) : cx.b == 256 ? fn<2>(__VA_ARGS__) : fn<1>(__VA_ARGS__))
 __device__ inline int getrf_item(const Ctx& cx, double* A, int* ipiv, double* LX, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) return TF_SLAB_RET(v_getrf_slab, cx, A, ipiv, LX);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) return TF_SLAB_RET(v_getrf_slab, cx, A, ipiv, LX, 0, cx.b);
   return v_getrf_ref(cx, A, ipiv, LX);
+}
+// GETRF slab task of the slab-level DAG (returns the first zero-pivot local column or -1).
+__device__ inline int getrf_slab_item(const Ctx& cx, double* A, int* ipiv, double* LX, int s, double* sm) {
+  return TF_SLAB_RET(v_getrf_slab, cx, A, ipiv, LX, s * NSR, (s + 1) * NSR);
 }
 TF_DEF_REF(v_trsmu, trsmu_item, (Ctx cx, const double* U, double* X, int item), (cx, U, X, item, dsm))
 TF_DEF_REF(v_xgemm, xgemm_item, (Ctx cx, const double* A, const double* B, double* C, int item),
@@ -1111,8 +1125,12 @@ TF_DEF_REF(v_ungessm, ungessm_item, (Ctx cx, const double* F, const int* ipiv, d
            (cx, F, ipiv, X, item, dsm))
 
 __device__ inline int tstrf_item(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) return TF_SLAB_RET(v_tstrf_slab, cx, U, A, Ls, ipiv);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) return TF_SLAB_RET(v_tstrf_slab, cx, U, A, Ls, ipiv, 0, cx.b);
   return v_tstrf_ref(cx, U, A, Ls, ipiv);
+}
+// TSTRF slab task of the slab-level DAG.
+__device__ inline int tstrf_slab_item(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, int s, double* sm) {
+  return TF_SLAB_RET(v_tstrf_slab, cx, U, A, Ls, ipiv, s * NSR, (s + 1) * NSR);
 }
 
 }  // namespace tf

@@ -573,7 +573,9 @@ __device__ inline int lu_panel(double* P, int ldp, int cs, int b, double* UL, in
 // U: the diagonal tile (upper region only is touched), A: the tile below, Ls: L strip,
 // ipiv: pivots (i,k).  Returns the first zero-pivot local column or -1.
 template <int MI>
-__device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, double* sm) {
+// Slabs [c_begin, c_end) only (the slab-level DAG's TSTRF slab tasks).
+__device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, int c_begin, int c_end,
+                                 double* sm) {
   const int b = cx.b, ib = cx.ib;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   constexpr int RW = 8 * MI;
@@ -582,7 +584,7 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
   int first_zero = -1;
   double acc[MI][SNJ][2];
   TF_LU_T0();
-  for (int cs = 0; cs < b; cs += NSR) {
+  for (int cs = c_begin; cs < c_end; cs += NSR) {
     const int s0 = cs - cs % ib, off = cs - s0;  // this slab's inner block and its offset in it
     slab_load<MI>(acc, A + (size_t)cs * b, b);
     {
@@ -657,7 +659,11 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
 // are then applied to the columns on its left (LAPACK dgetrf semantics, Z12).  LX: explicit
 // unit-lower copy written at the end.  Returns the first zero-pivot local column or -1.
 template <int MI>
-__device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX, double* sm) {
+// Slabs [c_begin, c_end) only (the slab-level DAG's GETRF slab tasks): between slab tasks the
+// running composition of the interchanges (tp) is parked in the first b ints of LX, which is
+// written only after the last slab.
+__device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX, int c_begin, int c_end,
+                                 double* sm) {
   const int b = cx.b, ib = cx.ib;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   constexpr int RW = 8 * MI;
@@ -665,9 +671,11 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
   const int ldp = b + 1;
   int first_zero = -1;
   double acc[MI][SNJ][2];
-  int tp = tid;  // running composition of the interchanges so far: row tid <- original row tp
+  int* tp_park = reinterpret_cast<int*>(LX);
+  // running composition of the interchanges so far: row tid <- original row tp
+  int tp = (c_begin > 0 && tid < b) ? ld_cg_int(tp_park + tid) : tid;
   TF_LU_T0();
-  for (int cs = 0; cs < b; cs += NSR) {
+  for (int cs = c_begin; cs < c_end; cs += NSR) {
     slab_load<MI>(acc, A + (size_t)cs * b, b);
     if (cs > 0) {
       lu_rows_permute<MI>(acc, ipiv, 0, cs, b, sm, tp);
@@ -747,6 +755,11 @@ __device__ inline int getrf_slab(const Ctx& cx, double* A, int* ipiv, double* LX
     }
     TF_LU_T(5);
   }
+  if (c_end < b) {
+    if (tid < b) tp_park[tid] = tp;
+    return first_zero;
+  }
+  __syncthreads();  // (every thread's parked tp was read before LX is overwritten)
   for (int e = tid; e < b * b; e += TF_THREADS) {
     const int r = e % b, cc = e / b;
     LX[e] = (r > cc) ? A[e] : (r == cc ? 1.0 : 0.0);

@@ -562,7 +562,10 @@ __device__ inline void slab_panel(double* P, int ldp, int cs, double* Rb, double
 // or TSQRT (ts = true: R = the diagonal tile's upper region, A = the tile below, VX unused),
 // left-looking over 32-column slabs.  Tst: the T strip (ib x b).
 template <int MI>
-__device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, double* Tst, double* VX, double* sm) {
+// Slabs [c_begin, c_end) only (multiples of 32): the slab-level DAG runs each slab as its own
+// task (a slab reads only global results of the slabs before it).
+__device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, double* Tst, double* VX, int c_begin,
+                               int c_end, double* sm) {
   const int b = cx.b, ib = cx.ib;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   constexpr int RW = 8 * MI;
@@ -573,7 +576,7 @@ __device__ inline void qr_slab(const Ctx& cx, bool ts, double* A, double* R, dou
 #ifdef TF_PROBE
   unsigned long long t0 = probe_now();
 #endif
-  for (int cs = 0; cs < b; cs += NSR) {
+  for (int cs = c_begin; cs < c_end; cs += NSR) {
     const int t = cs / NSR;
     slab_load<MI>(acc, A + (size_t)cs * b, b);
     // every finished reflector group, in order

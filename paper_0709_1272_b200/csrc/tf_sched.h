@@ -42,6 +42,15 @@ constexpr int ALG_GETRS = 3, ALG_ORMQR = 4, ALG_QRS = 5, ALG_LUN = 6;
 // tile column j has been copied in (a flag written by the copy stream); DONE(j) runs when
 // every tile of column j is final and sets the flag the D2H copy stream waits on
 constexpr int K_ARRIVE = 23, K_DONE = 24;
+// slab-level DAG (QR / LU on the register-slab path, single GPU): the panel tasks of
+// Algorithms 2-3 run as one task per 32-column slab (pad = slab), and the update tasks of
+// the next panel column (j = k + 1) as one task per slab item (pad = item offset), so that
+// consecutive TSQRT / TSTRF of a column and the next panel pipeline slab by slab
+// (DESIGN.md §6); the arithmetic of every tile is unchanged.
+constexpr int K_GEQRT_S = 25, K_TSQRT_S = 26, K_GETRF_S = 27, K_TSTRF_S = 28;
+TF_HD inline int coarse_kind(int kind) {
+  return kind == K_GEQRT_S ? 4 : kind == K_TSQRT_S ? 6 : kind == K_GETRF_S ? 8 : kind == K_TSTRF_S ? 10 : kind;
+}
 
 TF_HD inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
 

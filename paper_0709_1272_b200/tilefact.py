@@ -18,7 +18,9 @@ KINDS = {"potrf": 0, "trsm": 1, "syrk": 2, "gemm": 3, "geqrt": 4, "larfb": 5, "t
          "ssrfb": 7, "getrf": 8, "gessm": 9, "tstrf": 10, "ssssm": 11}
 SOLVE_KINDS = {"unitl": 14, "xgessm": 15, "xssssm": 16, "xlarfb": 17, "xssrfb": 18, "xtrsmu": 19, "xgemm": 20,
                "xunssssm": 21, "xungessm": 22}
+SLAB_KINDS = {"geqrt_s": 25, "tsqrt_s": 26, "getrf_s": 27, "tstrf_s": 28}  # slab-level DAG panel tasks
 KIND_NAMES = {v: k for k, v in KINDS.items()}
+KIND_NAMES.update({v: k for k, v in SLAB_KINDS.items()})
 ALGS = {"chol": 0, "qr": 1, "lu": 2, "getrs": 3, "ormqr": 4, "qrs": 5, "lu_apply_N": 6}
 
 
@@ -52,10 +54,12 @@ def _load():
         "tile_unpack": (i32, [i64, i64, i64, vp, vp, vp]),
         "tile_factor_host": (i32, [i32, i64, i64, i64, vp, vp, vp, vp, vp]),
         "tile_set_policy": (None, [i32]),
+        "tile_set_slab_dag": (None, [i32]),
         "tile_set_trace": (None, [i64]),
         "tile_trace_fetch": (i64, [vp, i64]),
         "tile_set_ctas": (None, [i32]),
         "tile_dag_export": (i64, [i32, i64, i32, vp, vp, vp, vp, vp, i64, vp, vp, i64, vp]),
+        "tile_dag_export_slab": (i64, [i32, i64, i64, i64, i32, vp, vp, vp, vp, vp, vp, i64, vp, vp, i64, vp]),
         "tk_run": (i32, [i32, i64, i64, vp, vp, vp, vp, vp, vp, vp]),
         "tile_dist_open": (i32, [i32, i64, i64, i64, i32, i32, i32, vp, vp]),
         "tile_dist_ipc_bytes": (i32, []),
@@ -85,8 +89,8 @@ SYMBOLS = [
     "tile_chol", "tile_qr", "tile_lu", "tile_qr_mn", "tile_lu_mn", "tile_mn_aux_elems", "tile_mn_ipiv_elems",
     "tile_lu_nopiv", "tile_getrs", "tile_ormqr", "tile_qrs", "tile_lu_apply_N",
     "tile_qr_t_elems", "tile_lu_l_elems", "tile_lu_ipiv_elems",
-    "tile_pack", "tile_unpack", "tile_factor_host", "tile_set_policy", "tile_set_trace",
-    "tile_trace_fetch", "tile_set_ctas", "tile_dag_export", "tk_run", "tile_dist_open",
+    "tile_pack", "tile_unpack", "tile_factor_host", "tile_set_policy", "tile_set_slab_dag", "tile_set_trace",
+    "tile_trace_fetch", "tile_set_ctas", "tile_dag_export", "tile_dag_export_slab", "tk_run", "tile_dist_open",
     "tile_dist_ipc_bytes", "tile_dist_connect", "tile_dist_factor", "tile_dist_close",
     "tile_dist_probe", "tile_dist_probe_read",
     "tile_dist_local_elems", "tile_dist_owner", "tile_dist_emulate", "tile_dist_plan_export",
@@ -272,6 +276,11 @@ def tile_set_policy(policy: int) -> None:
     lib.tile_set_policy(int(policy))
 
 
+def tile_set_slab_dag(on: int) -> None:
+    """1 = slab-level QR / LU task graph (default), 0 = tile-level, -1 = default."""
+    lib.tile_set_slab_dag(int(on))
+
+
 def tile_set_trace(cap: int) -> None:
     lib.tile_set_trace(int(cap))
 
@@ -304,6 +313,26 @@ def tile_dag_export(alg, p, policy=1):
     P = lambda x: ctypes.c_void_p(x.ctypes.data)  # noqa: E731
     lib.tile_dag_export(a, p, policy, P(cols["kind"]), P(cols["k"]), P(cols["i"]), P(cols["j"]),
                         P(cols["level"]), nt, P(off), P(succ), ne.value, ctypes.byref(ne))
+    cols["succ_off"] = off
+    cols["succ"] = succ[:ne.value]
+    return cols
+
+
+def tile_dag_export_slab(alg, p, b=128, ib=32, policy=1):
+    """Host-only: the slab-level task graph tile_qr / tile_lu run."""
+    import numpy as np
+    a = ALGS[alg] if isinstance(alg, str) else int(alg)
+    ne = ctypes.c_int64(0)
+    nt = lib.tile_dag_export_slab(a, p, b, ib, policy, None, None, None, None, None, None, 0, None, None, 0,
+                                  ctypes.byref(ne))
+    if nt < 0:
+        raise TileFactError("tile_dag_export_slab failed")
+    cols = {k: np.zeros(nt, dtype=np.int32) for k in ("kind", "k", "i", "j", "slab", "level")}
+    off = np.zeros(nt + 1, dtype=np.int64)
+    succ = np.zeros(max(1, ne.value), dtype=np.int32)
+    P = lambda x: ctypes.c_void_p(x.ctypes.data)  # noqa: E731
+    lib.tile_dag_export_slab(a, p, b, ib, policy, P(cols["kind"]), P(cols["k"]), P(cols["i"]), P(cols["j"]),
+                             P(cols["slab"]), P(cols["level"]), nt, P(off), P(succ), ne.value, ctypes.byref(ne))
     cols["succ_off"] = off
     cols["succ"] = succ[:ne.value]
     return cols

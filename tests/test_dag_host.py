@@ -383,3 +383,113 @@ def test_solve_dag_random_replay(alg):
     else:
         want = oracle.qr_solve(F, S, Y, n, b, ib)
     assert np.max(np.abs(ref - want)) <= 1e-10 * max(1.0, np.max(np.abs(want)))
+
+
+# ---------------------------------------------------------------- slab-level graph
+def _slab_rw(alg, kind, k, i, j, s, S, whole_items):
+    """Read / write regions of the slab-level tasks, independent of the builder: a tile is
+    split into 32-column slabs; a diagonal tile's slab into its upper (rows <= the slab's
+    last column) and lower parts; X = T strip / L strip + pivots of a slab, V = the
+    explicit V / L copy.  Regions are supersets where a kernel's exact footprint is finer
+    (GETRF's interchanges move lower-part rows of every earlier slab; an odd TSTRF slab
+    with ib = 64 rewrites rows of the slab before it; GETRF parks state in V)."""
+    lu = alg == "lu"
+    F, R, C, U = (4, 5, 6, 7) if alg == "qr" else (8, 9, 10, 11)
+    FS, CS = (25, 26) if alg == "qr" else (27, 28)
+
+    def tile(r, c, ss):
+        return [("lo", r, r, x) for x in ss] + [("up", r, r, x) for x in ss] if r == c else [("A", r, c, x) for x in ss]
+
+    allS = range(S)
+    if kind == FS:
+        # left-looking: the earlier slabs' multipliers / reflectors (lower parts, V) and their
+        # T / pivots; the upper parts (R / U) of earlier slabs are not read
+        rd = [("lo", k, k, x) for x in range(s)] + [("X", k, k, x) for x in range(s)] + \
+             [("V", k, x) for x in range(s)]
+        wr = [("up", k, k, s), ("lo", k, k, s), ("X", k, k, s)]
+        if lu:
+            wr += [("lo", k, k, x) for x in range(s)] + [("V", k, x) for x in allS]
+        else:
+            wr += [("V", k, s)]
+        return rd, wr
+    if kind == CS:
+        prev = [s - 1] if s > 0 else []
+        rd = [("up", k, k, s)] + [("A", i, k, x) for x in range(s)] + [("X", i, k, x) for x in range(s)]
+        wr = [("up", k, k, s), ("A", i, k, s), ("X", i, k, s)] + [("A", i, k, x) for x in prev] + \
+             [("X", i, k, x) for x in prev]
+        return rd, wr
+    items = allS if whole_items else [s]
+    if kind == R:
+        return [("V", k, x) for x in allS] + [("X", k, k, x) for x in allS], tile(k, j, items)
+    assert kind == U
+    return [("A", i, k, x) for x in allS] + [("X", i, k, x) for x in allS], tile(k, j, items) + tile(i, j, items)
+
+
+@pytest.mark.parametrize("alg,p,b", [("qr", 5, 128), ("lu", 5, 128), ("lu", 4, 256), ("qr", 3, 512)])
+def test_slab_dag_orders_every_hazard(alg, p, b):
+    """Soundness of the slab-level graph: in the builder's program order,
+    every read-after-write, write-after-read and write-after-write conflict of the
+    independent slab-region model above is ordered by a path of the exported graph; and
+    the graph has the expected tasks (panel tasks split per slab, next-column updates per
+    slab item)."""
+    d = tf.tile_dag_export_slab(alg, p, b, 32)
+    S = b // 32
+    nt = len(d["kind"])
+    F, R, C, U = (4, 5, 6, 7) if alg == "qr" else (8, 9, 10, 11)
+    FS, CS = (25, 26) if alg == "qr" else (27, 28)
+    kinds = [int(x) for x in d["kind"]]
+    # task census
+    assert kinds.count(FS) == p * S and kinds.count(CS) == S * p * (p - 1) // 2
+    n_split_r = sum(1 for t in range(nt) if kinds[t] == R and d["j"][t] == d["k"][t] + 1)
+    assert n_split_r == (p - 1) * S
+    pr = _preds(d)
+    # whole update tasks: j > k + 1 (one task, S items)
+    whole = [kinds[t] in (R, U) and d["j"][t] > d["k"][t] + 1 for t in range(nt)]
+    last_w, readers, hazards = {}, {}, []
+    for t in range(nt):
+        rd, wr = _slab_rw(alg, kinds[t], int(d["k"][t]), int(d["i"][t]), int(d["j"][t]), int(d["slab"][t]), S,
+                          whole[t])
+        h = set()
+        for r in rd + wr:
+            if r in last_w:
+                h.add(last_w[r])
+        for r in wr:
+            h.update(readers.get(r, ()))
+        h.discard(t)
+        hazards.append(h)
+        for r in rd:
+            readers.setdefault(r, set()).add(t)
+        for r in wr:
+            last_w[r] = t
+            readers[r] = set()
+    # ancestors by a forward pass (program order is a topological order of the graph)
+    anc = [set() for _ in range(nt)]
+    for t in range(nt):
+        for u in pr[t]:
+            assert u < t, "edges follow program order"
+            anc[t] |= anc[u] | {u}
+        missing = hazards[t] - anc[t]
+        assert not missing, (t, kinds[t], int(d["k"][t]), int(d["i"][t]), int(d["j"][t]), int(d["slab"][t]),
+                             [(kinds[u], int(d["k"][u]), int(d["i"][u]), int(d["j"][u]), int(d["slab"][u]))
+                              for u in missing])
+
+
+def test_slab_dag_shorter_chains():
+    """The slab-level graph's longest path in slab-steps (panel slab = 1, update item = 1)
+    is much shorter than the tile-level graph's (a tile panel = S steps): consecutive
+    TSTRF of a column pipeline slab by slab."""
+    p, b = 16, 256
+    S = b // 32
+    d = tf.tile_dag_export_slab("lu", p, b, 32)
+    pr = _preds(d)
+    L = np.zeros(len(pr))
+    for t in range(len(pr)):
+        L[t] = 1 + max((L[u] for u in pr[t]), default=0)
+    fine = L.max()
+    c = tf.tile_dag_export("lu", p)
+    prc = _preds(c)
+    Lc = np.zeros(len(prc))
+    for t in range(len(prc)):
+        w = S if int(c["kind"][t]) in (8, 10) else 1
+        Lc[t] = w + max((Lc[u] for u in prc[t]), default=0)
+    assert fine < 0.65 * Lc.max(), (fine, Lc.max())  # 158 vs 263 slab-steps at p = 16, S = 8

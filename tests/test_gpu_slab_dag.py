@@ -1,0 +1,74 @@
+"""GPU: the slab-level task graph (tile_set_slab_dag) gives results bitwise
+identical to the paper's tile-level graph: every tile sees the same
+kernel operations in the same order, only the granularity of the dependencies changes.
+Factors, T / L strips, pivots and info are compared bit for bit, over square and
+rectangular tile grids, ib = 32 and 64, and a singular LU (info from a slab task)."""
+import numpy as np
+import pytest
+import torch
+
+import tilegen
+from _gpu_util import gpu_factor, gpu_pack
+from paper_0709_1272_b200 import tilefact as tf
+
+pytestmark = pytest.mark.gpu
+
+
+def _both(fn):
+    out = []
+    for on in (0, 1):
+        tf.tile_set_slab_dag(on)
+        try:
+            out.append(fn())
+        finally:
+            tf.tile_set_slab_dag(-1)
+    return out
+
+
+@pytest.mark.parametrize("alg,n,b,ib,seed", [("qr", 1024, 256, 32, 0), ("lu", 1024, 256, 32, 1),
+                                             ("qr", 1536, 512, 64, 2), ("lu", 1536, 512, 64, 3),
+                                             ("qr", 640, 128, 32, 4), ("lu", 640, 128, 64, 5),
+                                             ("lu", 2048, 256, 64, 6)])
+def test_slab_dag_bitwise_equals_tile_dag(alg, n, b, ib, seed):
+    A = (tilegen.uniform if alg == "qr" else tilegen.normal)(n, seed)
+    (G0, X0, P0, i0), (G1, X1, P1, i1) = _both(lambda: gpu_factor(alg, A, b, ib))
+    assert np.array_equal(G0.view(np.int64), G1.view(np.int64))
+    assert np.array_equal(X0.view(np.int64), X1.view(np.int64))
+    if alg == "lu":
+        assert np.array_equal(P0, P1)
+    assert i0 == i1 == 0
+
+
+def test_slab_dag_singular_lu_info():
+    n, b, ib = 768, 256, 32
+    A = tilegen.normal(n, 7)
+    A[:, 300] = 0.0  # a zero column inside slab 1 of tile column 1
+    (G0, _, P0, i0), (G1, _, P1, i1) = _both(lambda: gpu_factor("lu", A, b, ib))
+    assert i0 == i1 and i0 > 0
+    assert np.array_equal(P0, P1)
+
+
+@pytest.mark.parametrize("alg,m,n,b,ib", [("qr", 1536, 768, 256, 32), ("lu", 1536, 768, 256, 32),
+                                          ("qr", 768, 1536, 256, 64), ("lu", 1024, 512, 128, 32)])
+def test_slab_dag_rectangular_bitwise(alg, m, n, b, ib):
+    rng = np.random.default_rng(11)
+    A = rng.uniform(-0.5, 0.5, (m, n)) if alg == "qr" else rng.standard_normal((m, n))
+
+    def run():
+        T = gpu_pack(A, b)
+        aux = torch.zeros(tf.tile_mn_aux_elems(m, n, b, ib), dtype=torch.float64, device="cuda")
+        if alg == "qr":
+            tf.tile_qr_mn(m, n, b, ib, T, aux)
+            piv = None
+        else:
+            piv = torch.zeros(tf.tile_mn_ipiv_elems(m, n, b), dtype=torch.int32, device="cuda")
+            info = torch.zeros(1, dtype=torch.int32, device="cuda")
+            tf.tile_lu_mn(m, n, b, ib, T, aux, piv, info)
+        torch.cuda.synchronize()
+        return T.cpu().numpy(), aux.cpu().numpy(), None if piv is None else piv.cpu().numpy()
+
+    (G0, X0, P0), (G1, X1, P1) = _both(run)
+    assert np.array_equal(G0.view(np.int64), G1.view(np.int64))
+    assert np.array_equal(X0.view(np.int64), X1.view(np.int64))
+    if P0 is not None:
+        assert np.array_equal(P0, P1)

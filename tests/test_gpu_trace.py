@@ -2,8 +2,8 @@
 PAPER.md:1014-1026; SPEC.md:360-366 trace validation) checked against the task graph.
 
 With tile_set_trace on, every work item records (task, item, SM, start_ns, end_ns) from
-%globaltimer.  For every edge u -> t of the exported DAG (tile_dag_export, the same graph
-the scheduler runs), no item of t may start before every item of u has ended, and every
+%globaltimer.  For every edge u -> t of the exported DAG (tile_dag_export, or for QR / LU
+on the register-slab sizes tile_dag_export_slab: the same graph the scheduler runs), no item of t may start before every item of u has ended, and every
 task's items must all be present exactly once.
 """
 import numpy as np
@@ -21,17 +21,21 @@ from _gpu_util import gpu_factor  # noqa: E402
 from paper_0709_1272_b200 import tilefact as tf  # noqa: E402
 
 
-@pytest.mark.parametrize("alg,n,b,ib", [("chol", 1024, 128, 32), ("qr", 1024, 256, 32), ("lu", 1024, 256, 32),
-                                        ("chol", 2048, 512, 64)])
-def test_trace_respects_dag(alg, n, b, ib):
+@pytest.mark.parametrize("alg,n,b,ib,slab", [("chol", 1024, 128, 32, 0), ("qr", 1024, 256, 32, 1),
+                                             ("lu", 1024, 256, 32, 1), ("qr", 1024, 256, 32, 0),
+                                             ("lu", 1024, 256, 32, 0), ("lu", 1536, 512, 64, 1),
+                                             ("chol", 2048, 512, 64, 0)])
+def test_trace_respects_dag(alg, n, b, ib, slab):
     A = {"chol": tilegen.spd, "qr": tilegen.uniform, "lu": tilegen.normal}[alg](n, 3)
     tf.tile_set_trace(1 << 22)
+    tf.tile_set_slab_dag(slab)
     try:
         gpu_factor(alg, A, b, ib)
         rec = tf.tile_trace_fetch()
     finally:
         tf.tile_set_trace(0)
-    d = tf.tile_dag_export(alg, n // b)
+        tf.tile_set_slab_dag(-1)
+    d = tf.tile_dag_export_slab(alg, n // b, b, ib) if slab else tf.tile_dag_export(alg, n // b)
     nt = len(d["kind"])
     task, item, start, end = rec[:, 0], rec[:, 1], rec[:, 3], rec[:, 4]
     assert len(rec) > 0 and (end >= start).all()

@@ -79,7 +79,8 @@ def main():
     bench.factor(tf, cfg, work, aux, piv, info)
     rec = tf.tile_trace_fetch()
     tf.tile_set_trace(0)
-    d = tf.tile_dag_export(cfg["kind"], n // b, a.policy)
+    fine = cfg["kind"] != "chol" and os.environ.get("TF_FINE", "1") != "0" and b in (128, 256, 512) and ib in (32, 64)
+    d = tf.tile_dag_export_slab(cfg["kind"], n // b, b, ib, a.policy) if fine else tf.tile_dag_export(cfg["kind"], n // b, a.policy)
     kinds = d["kind"][rec[:, 0]]
     t0 = rec[:, 3].min()
     start = (rec[:, 3] - t0) / 1e3
@@ -87,7 +88,7 @@ def main():
     dur = end - start
     span = end.max()
     nsm = len(np.unique(rec[:, 2]))
-    out = {"config": cfg["desc"], "n": n, "b": b, "ib": ib, "ms_untraced": ms, "ms_traced_span": span / 1e3,
+    out = {"config": cfg["desc"], "dag": "slab" if fine else "tile", "n": n, "b": b, "ib": ib, "ms_untraced": ms, "ms_traced_span": span / 1e3,
            "gflops_untraced": bench.lapack_flops(cfg["kind"], n) / (ms * 1e-3) / 1e9,
            "sms": nsm, "items": len(rec), "busy_frac": float(dur.sum() / (nsm * span)), "kinds": {}}
     # gaps between consecutive items on each SM
@@ -104,7 +105,10 @@ def main():
         name = tf.KIND_NAMES[int(kid)]
         m = kinds == kid
         nit = int(rec[m, 1].max()) + 1  # items per task of this kind
-        fl = item_flops(name, b, ib, nit)
+        if name.endswith("_s"):  # slab-level panel task: one 32-column slab of the tile
+            fl = item_flops(name[:-2], b, ib, b // 32)
+        else:
+            fl = item_flops(name, b, ib, max(nit, b // 32) if name in ("larfb", "ssrfb", "gessm", "ssssm") else nit)
         out["kinds"][name] = {"items": int(m.sum()), "mean_us": float(dur[m].mean()), "max_us": float(dur[m].max()),
                               "gflops_per_sm": float(fl / (dur[m].mean() * 1e-6) / 1e9),
                               "sm_time_share": float(dur[m].sum() / dur.sum())}

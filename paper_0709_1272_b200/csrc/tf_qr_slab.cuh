@@ -224,8 +224,14 @@ __device__ __forceinline__ void slab_store(const double (&acc)[MI][SNJ][2], doub
 // reduction through shared memory and no barrier per 16 W rows), the two group partials are
 // added in a fixed order (group 0's + group 1's).  Then W2 = T_s^T (R_s + W) (DMMA),
 // R_s -= W2, A -= V_s W2 on the accumulators, and the mirror rows are refreshed.
-constexpr int MIR_LD = NSR;  // mirror row length (doubles), swizzled
-__device__ __forceinline__ int mir_idx(int r, int c) { return r * MIR_LD + (c ^ ((r & 3) << 2)); }
+// Mirror layout: row r holds slab row r (32 doubles) with column c at slot (c & 7) * 4 +
+// (c >> 3), so the four B-fragment values a lane of group g needs for one k-step (columns
+// g, 8 + g, 16 + g, 24 + g) are adjacent (two 128-bit loads); the 16-byte chunks of a row
+// are XOR-swizzled by its low two bits so the 8 lanes of each load phase (4 rows x 2 lane
+// groups) hit 8 distinct bank groups.
+constexpr int MIR_LD = NSR;  // mirror row length (doubles)
+__device__ __forceinline__ int mir_sw(int r) { return ((r & 1) << 2) | ((r >> 1) & 1); }
+__device__ __forceinline__ int mir_chunk(int r, int chunk) { return r * MIR_LD + ((chunk ^ mir_sw(r)) << 1); }
 
 template <int MI>
 __device__ inline void ssrfb_mirror(const Ctx& cx, const double* V, const double* Tst, double* R, double* A, int item,
@@ -243,16 +249,28 @@ __device__ inline void ssrfb_mirror(const Ctx& cx, const double* V, const double
   double acc[MI][SNJ][2];
   slab_load<MI>(acc, A, b);
   auto mirror = [&]() {
+    // element (r, 8j + 2q + e): slot ((2q + e) << 2) | j, so j = 2m, 2m + 1 share chunk
+    // 4q + 2e + m.  Store x of lane q writes combination (e, m) = (x + q) & 3, so the four
+    // lanes of a row hit four different bank groups (with the row swizzle: all 8 lanes of
+    // a store phase distinct)
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < SNJ; ++j)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) sMir[mir_idx(r0 + 8 * i + g, 8 * j + 2 * q + e)] = acc[i][j][e];
+      for (int x = 0; x < 4; ++x) {
+        const int cmb = (x + q) & 3, e = cmb >> 1, m = cmb & 1;
+        const double v0 = e ? (m ? acc[i][2][1] : acc[i][0][1]) : (m ? acc[i][2][0] : acc[i][0][0]);
+        const double v1 = e ? (m ? acc[i][3][1] : acc[i][1][1]) : (m ? acc[i][3][0] : acc[i][1][0]);
+        *reinterpret_cast<double2*>(sMir + mir_chunk(r0 + 8 * i + g, (q << 2) | cmb)) = make_double2(v0, v1);
+      }
   };
   mirror();
   const int grp = warp >> 3, wg = warp & 7;
   const int kh = b / 2, k0g = grp * kh;     // this group's rows of the W reduction
+  // W tile of this warp: m-block mb, n-blocks nb0 .. nb0+NB-1 (ib = 64: 8 x 32; ib = 32: 8 x 16)
+  constexpr int NBMAX = 4;
+  const int NB = ib == 64 ? 4 : 2;
+  const int mb = ib == 64 ? wg : (wg >> 1), nb0 = ib == 64 ? 0 : 2 * (wg & 1);
+  const double* vcol0 = V + (size_t)(8 * mb + g) * b + k0g + q;  // + c0 b: V(k0g + 4ks + q, c0 + 8mb + g)
   for (int c0 = 0; c0 < b; c0 += ib) {
     const int nw = ib;
     const double* Vs = V + (size_t)c0 * b;
@@ -271,17 +289,19 @@ __device__ inline void ssrfb_mirror(const Ctx& cx, const double* V, const double
     __syncthreads();  // the mirror holds this block's input slab
     TF_LU_T0();
     // ---- W (nw x 32) over this group's rows: warp wg owns m-block mb, n-blocks nb0 .. nb0+NB-1
-    constexpr int NBMAX = 4;
-    const int NB = nw == 64 ? 4 : 2;
-    const int mb = nw == 64 ? wg : (wg >> 1), nb0 = nw == 64 ? 0 : 2 * (wg & 1);
     double w[NBMAX][2];
 #pragma unroll
     for (int x = 0; x < NBMAX; ++x) w[x][0] = w[x][1] = 0.0;
-    const double* vcol = Vs + (size_t)(8 * mb + g) * b + k0g + q;  // V(k0g + 4ks + q, 8mb + g)
+    const double* vcol = vcol0 + (size_t)c0 * b;
     // V operand 8 k-steps at a time, the next group in flight while this one is used
     double av[8], avn[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) avn[u] = vcol[4 * u];
+    // this lane's mirror rows k0g + 4 ks + q (low bits q: a fixed swizzle), its chunks
+    // (g << 1) | (n-block >> 1): addresses are the row base + immediates
+    const double* mrow = sMir + (size_t)(k0g + q) * MIR_LD;
+    const int sw = mir_sw(q);
+    const int off0 = (((g << 1) | (nb0 >> 1)) ^ sw) << 1, off1 = (((g << 1) | 1) ^ sw) << 1;
 #pragma unroll 1
     for (int ks0 = 0; ks0 < kh / 4; ks0 += 8) {
 #pragma unroll
@@ -290,12 +310,24 @@ __device__ inline void ssrfb_mirror(const Ctx& cx, const double* V, const double
 #pragma unroll
         for (int u = 0; u < 8; ++u) avn[u] = vcol[4 * (ks0 + 8 + u)];
       }
+      const double* rp = mrow + (size_t)ks0 * 4 * MIR_LD;
+      if (NB == 4) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = k0g + 4 * (ks0 + u) + q;
+        for (int u = 0; u < 8; ++u) {
+          const double2 lo = *reinterpret_cast<const double2*>(rp + u * 4 * MIR_LD + off0);
+          const double2 hi = *reinterpret_cast<const double2*>(rp + u * 4 * MIR_LD + off1);
+          dmma(w[0], av[u], lo.x);
+          dmma(w[1], av[u], lo.y);
+          dmma(w[2], av[u], hi.x);
+          dmma(w[3], av[u], hi.y);
+        }
+      } else {
 #pragma unroll
-        for (int x = 0; x < NBMAX; ++x)
-          if (x < NB) dmma(w[x], av[u], sMir[mir_idx(k, 8 * (nb0 + x) + g)]);
+        for (int u = 0; u < 8; ++u) {
+          const double2 lo = *reinterpret_cast<const double2*>(rp + u * 4 * MIR_LD + off0);
+          dmma(w[0], av[u], lo.x);
+          dmma(w[1], av[u], lo.y);
+        }
       }
     }
     TF_LU_T(24);

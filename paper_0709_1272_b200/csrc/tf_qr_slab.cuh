@@ -459,8 +459,11 @@ __device__ inline void slab_panel(double* P, int ldp, int cs, double* Rb, double
   constexpr int RW = 8 * MI;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = lane, r0w = warp * RW;
-  double* part = sm2;          // 2 x 16 x 32 warp partials
-  double* sS = part + 1024;    // 32 x 33: sdot_m of column jj (m < jj), for the T recurrence
+  constexpr int PLD = 18;      // partials stored transposed: lane c's 16 warp partials at
+                               // part[c * PLD + w] (two 128-bit loads per pair of warps,
+                               // 16-byte chunks of the 8 lanes of a load phase distinct)
+  double* part = sm2;          // 2 x 32 x PLD warp partials
+  double* sS = part + 2 * 32 * PLD;  // 32 x 33: sdot_m of column jj (m < jj), for the T recurrence
   double* sTau = sS + 32 * 33; // 32 taus
   double* sTop = sTau + 32;    // GEQRT: 2 x 32 top rows (by column parity)
   double* Rbn = sTop + 64;     // TSQRT: 32 x 33 finished R rows (Rb stays read-only)
@@ -506,17 +509,19 @@ __device__ inline void slab_panel(double* P, int ldp, int cs, double* Rb, double
         if (k == kcg) tv = p[k];
       top_row[c] = tv;
     }
-    double* pb = part + (jj & 1) * 512;
-    pb[warp * 32 + c] = d0 + d1;
+    double* pb = part + (jj & 1) * 32 * PLD;
+    pb[c * PLD + warp] = d0 + d1;
     __syncthreads();
     // every warp: column sums (fixed order), Householder scalars, w_c of its lane's column
     double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
 #pragma unroll
     for (int w = 0; w < TF_WARPS; w += 4) {
-      e0 += pb[w * 32 + c];
-      e1 += pb[(w + 1) * 32 + c];
-      e2 += pb[(w + 2) * 32 + c];
-      e3 += pb[(w + 3) * 32 + c];
+      const double2 v01 = *reinterpret_cast<const double2*>(pb + c * PLD + w);
+      const double2 v23 = *reinterpret_cast<const double2*>(pb + c * PLD + w + 2);
+      e0 += v01.x;
+      e1 += v01.y;
+      e2 += v23.x;
+      e3 += v23.y;
     }
     const double dd = (e0 + e1) + (e2 + e3);
     const double ss = __shfl_sync(0xffffffffu, dd, jj);
@@ -539,19 +544,23 @@ __device__ inline void slab_panel(double* P, int ldp, int cs, double* Rb, double
     }
     // rank-1 update: p <- fac*p - tw*(x*rden); lane jj (tw = 0, fac = rden) becomes v
     const double fac = (c == jj) ? rden : 1.0;
+    auto xk = [&](int k) -> double2 { return *reinterpret_cast<const double2*>(xw + k); };
+    // (tw rden) x instead of tw (x rden): two FP64 operations per element instead of three
+    // (the panel is bound by the FP64 pipe and its latency chain; rounding-level change)
+    const double twr = tw * rden;
     if (full) {
 #pragma unroll
       for (int k = 0; k < RW; k += 2) {
-        const double2 x2 = *reinterpret_cast<const double2*>(xw + k);
-        p[k] = fma(-tw, x2.x * rden, p[k] * fac);
-        p[k + 1] = fma(-tw, x2.y * rden, p[k + 1] * fac);
+        const double2 x2 = xk(k);
+        p[k] = fma(-twr, x2.x, p[k] * fac);
+        p[k + 1] = fma(-twr, x2.y, p[k + 1] * fac);
       }
     } else if (!none) {
 #pragma unroll
       for (int k = 0; k < RW; k += 2) {
-        const double2 x2 = *reinterpret_cast<const double2*>(xw + k);
-        if (k > kcg) p[k] = fma(-tw, x2.x * rden, p[k] * fac);
-        if (k + 1 > kcg) p[k + 1] = fma(-tw, x2.y * rden, p[k + 1] * fac);
+        const double2 x2 = xk(k);
+        if (k > kcg) p[k] = fma(-twr, x2.x, p[k] * fac);
+        if (k + 1 > kcg) p[k + 1] = fma(-twr, x2.y, p[k + 1] * fac);
       }
       if (kcg >= 0) {  // GEQRT top row: R entries of row cg
 #pragma unroll

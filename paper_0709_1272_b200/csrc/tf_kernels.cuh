@@ -140,7 +140,46 @@ __device__ inline void load_ts(double* sT, const double* Tst, int ib, int c0) {
 
 // In-place Cholesky of the nb x nb lower block D (smem, ld NB+1) by warp 0, left-looking
 // per column as in DPOTF2.  Returns -1 or the failing local column.
+// nb = NB: fully unrolled, lane i keeps its row in registers, row j's finished values come
+// as shared-memory broadcasts (independent loads, issued as soon as column j-1 is stored),
+// four interleaved partial sums (the dependent chain per column is ~j/4 FMAs + rsqrt).
+// (A register-resident right-looking variant with the multipliers by shuffles was measured
+// slower: 496 shuffles issue from one warp; potrf b=128 63 -> 136 us.)
 __device__ inline int chol_diag_block(double* D, int nb, int* sflag) {
+  if (nb == NB) {
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      double x[NB];
+#pragma unroll
+      for (int c = 0; c < NB; ++c) x[c] = c <= lane ? D[lane + c * (NB + 1)] : 0.0;
+      int fail = -1;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        double p[4] = {x[j], 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int m = 0; m < j; ++m) p[m & 3] -= x[m] * D[j + m * (NB + 1)];
+        const double sj = (p[0] + p[1]) + (p[2] + p[3]);
+        const double d = __shfl_sync(0xffffffffu, sj, j);
+        if (!(d > 0.0)) {
+          fail = j;
+          break;
+        }
+        const double r = rsqrt(d);
+        if (lane == j) {
+          x[j] = d * r;
+          D[j + j * (NB + 1)] = x[j];
+          D[NB + j * (NB + 1)] = r;  // padding row: reciprocal of L_jj for row_solve
+        } else if (lane > j) {
+          x[j] = sj * r;
+          D[lane + j * (NB + 1)] = x[j];
+        }
+        __syncwarp();
+      }
+      if (lane == 0) *sflag = fail;
+    }
+    __syncthreads();
+    return *sflag;
+  }
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
     int fail = -1;
@@ -286,6 +325,147 @@ __device__ inline int potrf_right(const Ctx& cx, double* A, double* sm) {
   return -1;
 }
 
+// ---- b = 128 (config 1's tile size): POTRF and TRSM entirely in shared memory.  The tile
+// is read once and written once; per 32-column block: warp 0's Cholesky of the diagonal
+// block (chol_diag_block), row solves against it, and the rank-32 update of what remains
+// by DMMA fragments read straight from shared memory (right-looking) — no global round
+// trips and no operand pipeline start-up inside the tile.  Same operations per element as
+// the blocked kernels above (products exact on the integer pins); rounding order differs.
+constexpr int T128_LD = 132;  // column stride: the 32 lanes of a fragment load hit 16 banks twice
+
+// row_solve on rows held in shared memory (X ld ldx), nb = NB
+__device__ inline void row_solve_smem(double* X, int ldx, int rows, const double* D) {
+  for (int r = threadIdx.x; r < rows; r += TF_THREADS) {
+    double x[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) x[c] = X[r + c * ldx];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      x[c] = x[c] * D[NB + c * (NB + 1)];
+#pragma unroll
+      for (int c2 = c + 1; c2 < NB; ++c2) x[c2] -= x[c] * D[c2 + c * (NB + 1)];
+    }
+#pragma unroll
+    for (int c = 0; c < NB; ++c) X[r + c * ldx] = x[c];
+  }
+}
+
+// C(8x8 fragment at rows r, columns cc of S, ld lds) -= sum_{k<32} A(r.., k) B(cc.., k), the
+// A / B columns k at A + k * lda / B + k * ldb (one warp)
+__device__ __forceinline__ void frag_rank32(double* S, int lds, int r, int cc, const double* Ak, int lda,
+                                            const double* Bk, int ldb) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  double c2[2] = {S[(r + g) + (size_t)(cc + 2 * q) * lds], S[(r + g) + (size_t)(cc + 2 * q + 1) * lds]};
+  double a[8], bv[8];
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    a[ks] = Ak[(r + g) + (size_t)(4 * ks + q) * lda];
+    bv[ks] = Bk[(cc + g) + (size_t)(4 * ks + q) * ldb];
+  }
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) dmma(c2, -a[ks], bv[ks]);
+  S[(r + g) + (size_t)(cc + 2 * q) * lds] = c2[0];
+  S[(r + g) + (size_t)(cc + 2 * q + 1) * lds] = c2[1];
+}
+
+__device__ inline int potrf_128(const Ctx& cx, double* A, double* sm) {
+  constexpr int LD = T128_LD;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  double* T = sm;                          // 128 x LD
+  double* D = T + 128 * LD;                // (NB+1) x NB
+  int* sflag = reinterpret_cast<int*>(D + (NB + 1) * NB);
+  TF_LU_T0();
+  for (int e = tid; e < 128 * 64; e += TF_THREADS) {  // lower triangle (upper: zeros)
+    const int r = (2 * e) % 128, c = (2 * e) / 128;
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(A + r + (size_t)c * 128));
+    T[r + c * LD] = r >= c ? v.x : 0.0;
+    T[r + 1 + c * LD] = r + 1 >= c ? v.y : 0.0;
+  }
+  __syncthreads();
+  for (int jb = 0; jb < 128; jb += NB) {
+    for (int e = tid; e < NB * NB; e += TF_THREADS) {
+      const int r = e % NB, c = e / NB;
+      D[r + c * (NB + 1)] = r >= c ? T[jb + r + (jb + c) * LD] : 0.0;
+    }
+    __syncthreads();
+    TF_LU_T(0);
+    const int fail = chol_diag_block(D, NB, sflag);
+    TF_LU_T(1);
+    if (fail >= 0) return jb + fail;
+    for (int e = tid; e < NB * NB; e += TF_THREADS) {
+      const int r = e % NB, c = e / NB;
+      if (r >= c) T[jb + r + (jb + c) * LD] = D[r + c * (NB + 1)];
+    }
+    const int m0 = jb + NB, m = 128 - m0;
+    if (m == 0) break;
+    row_solve_smem(T + m0 + jb * LD, LD, m, D);
+    __syncthreads();
+    TF_LU_T(2);
+    // trailing lower triangle (8x8 fragments on and below the block diagonal)
+    const int nbk = m / 8, nfrag = nbk * (nbk + 1) / 2;
+    for (int f = warp; f < nfrag; f += TF_WARPS) {
+      int bi = (int)((sqrtf(8.0f * f + 1.0f) - 1.0f) * 0.5f);
+      while ((bi + 1) * (bi + 2) / 2 <= f) ++bi;
+      while (bi * (bi + 1) / 2 > f) --bi;
+      const int bj = f - bi * (bi + 1) / 2;
+      frag_rank32(T, LD, m0 + 8 * bi, m0 + 8 * bj, T + jb * LD, LD, T + jb * LD, LD);
+    }
+    __syncthreads();
+    TF_LU_T(3);
+  }
+  __syncthreads();
+  for (int e = tid; e < 128 * 128; e += TF_THREADS) {
+    const int r = e % 128, c = e / 128;
+    if (r >= c) A[r + (size_t)c * 128] = T[r + c * LD];
+  }
+  return -1;
+}
+
+// TRSM, b = 128: X (128 x 128) <- X L^{-T} in shared memory, right-looking over 32-column
+// blocks: row solves of block jb against L's diagonal block, then X(:, jb+32:) -= X(:, jb
+// block) L(jb+32:, jb block)^T by DMMA fragments from shared memory.
+__device__ inline void trsm_128(const Ctx& cx, const double* L, double* X, double* sm) {
+  constexpr int LD = T128_LD;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  double* Xs = sm;                        // 128 x LD
+  double* Ls = Xs + 128 * LD;             // L(jb.., jb block): 32 columns, ld LD
+  double* D = Ls + NB * LD;               // (NB+1) x NB
+  for (int e = tid; e < 128 * 64; e += TF_THREADS) {
+    const int r = (2 * e) % 128, c = (2 * e) / 128;
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(X + r + (size_t)c * 128));
+    Xs[r + c * LD] = v.x;
+    Xs[r + 1 + c * LD] = v.y;
+  }
+  for (int jb = 0; jb < 128; jb += NB) {
+    const int rows = 128 - jb;  // L rows jb .. 127 of the block's columns
+    for (int e = tid; e < rows * NB; e += TF_THREADS) {
+      const int r = e % rows, c = e / rows;
+      Ls[r + c * LD] = ldg_cg(L + (jb + r) + (size_t)(jb + c) * 128);
+    }
+    __syncthreads();
+    for (int e = tid; e < NB * NB; e += TF_THREADS) {
+      const int r = e % NB, c = e / NB;
+      const double v = r >= c ? Ls[r + c * LD] : 0.0;
+      D[r + c * (NB + 1)] = v;
+      if (r == c) D[NB + c * (NB + 1)] = 1.0 / v;
+    }
+    __syncthreads();
+    row_solve_smem(Xs + jb * LD, LD, 128, D);
+    __syncthreads();
+    const int n0 = jb + NB, ncol = 128 - n0;
+    const int nfrag = 16 * (ncol / 8);
+    for (int f = warp; f < nfrag; f += TF_WARPS) {
+      const int bi = f % 16, bj = f / 16;
+      frag_rank32(Xs, LD, 8 * bi, n0 + 8 * bj, Xs + jb * LD, LD, Ls - jb, LD);  // L(row, jb + k) = Ls[row - jb + k LD]
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < 128 * 64; e += TF_THREADS) {
+    const int r = (2 * e) % 128, c = (2 * e) / 128;
+    *reinterpret_cast<double2*>(X + r + (size_t)c * 128) = make_double2(Xs[r + c * LD], Xs[r + 1 + c * LD]);
+  }
+}
+
 // TRSM (DTRSM): rows [item*RB, +RB) of X <- X L^{-T}, left-looking over
 // column blocks of NB: X[:,cb] -= X[:,<cb] L[cb,<cb]^T (DMMA), then the NB x NB solve.
 __device__ inline void trsm_left(const Ctx& cx, const double* L, double* X, int item, double* sm) {
@@ -415,6 +595,8 @@ TF_DEF_REF_RET(v_potrf_left, potrf_left, (Ctx cx, double* A), (cx, A, dsm))
 TF_DEF_REF_RET(v_potrf_right, potrf_right, (Ctx cx, double* A), (cx, A, dsm))
 TF_DEF_REF(v_trsm_left, trsm_left, (Ctx cx, const double* L, double* X, int item), (cx, L, X, item, dsm))
 TF_DEF_REF(v_trsm_right, trsm_right, (Ctx cx, const double* L, double* X, int item), (cx, L, X, item, dsm))
+TF_DEF_REF_RET(v_potrf_128, potrf_128, (Ctx cx, double* A), (cx, A, dsm))
+TF_DEF_REF(v_trsm_128, trsm_128, (Ctx cx, const double* L, double* X), (cx, L, X, dsm))
 TF_DEF_REF(v_syrk, syrk_body, (Ctx cx, const double* A, double* C, int item), (cx, A, C, item, dsm))
 TF_DEF_REF(v_gemm, gemm_body, (Ctx cx, const double* A, const double* B, double* C, int item), (cx, A, B, C, item, dsm))
 
@@ -422,11 +604,13 @@ TF_DEF_REF(v_gemm, gemm_body, (Ctx cx, const double* A, const double* B, double*
 // variants re-declare it).  POTRF / TRSM: right-looking over 128-column panels for b a
 // multiple of 128 (>= 256), left-looking 32-column blocks otherwise.
 __device__ inline int potrf_item(const Ctx& cx, double* A, double*) {
+  if (cx.b == 128) return v_potrf_128(cx, A);
   if (cx.b < 256 || cx.b % 128) return v_potrf_left(cx, A);
   return v_potrf_right(cx, A);
 }
 __device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int item, double*) {
-  if (cx.b < 256 || cx.b % 128) v_trsm_left(cx, L, X, item);
+  if (cx.b == 128) v_trsm_128(cx, L, X);
+  else if (cx.b < 256 || cx.b % 128) v_trsm_left(cx, L, X, item);
   else v_trsm_right(cx, L, X, item);
 }
 __device__ inline void syrk_item(const Ctx& cx, const double* A, double* C, int item, double*) { v_syrk(cx, A, C, item); }

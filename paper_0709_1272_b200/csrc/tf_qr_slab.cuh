@@ -315,6 +315,10 @@ __device__ inline void ssrfb_mirror(const Ctx& cx, const double* V, const double
       }
     }
     TF_LU_T(24);
+    // the update's first V k-step, in flight through the reduction and W2
+    double an[MI];
+#pragma unroll
+    for (int i = 0; i < MI; ++i) an[i] = Vs[(r0 + 8 * i + g) + (size_t)q * b];
     // group 1 -> shared memory, group 0 adds (fixed order: group 0 + group 1)
     if (grp == 1) {
 #pragma unroll
@@ -372,9 +376,6 @@ __device__ inline void ssrfb_mirror(const Ctx& cx, const double* V, const double
     {
       // (the sign is applied at the DMMA, where it folds into the operand modifier; negating
       // at load time costs a DADD on the FP64 pipe the DMMAs share)
-      double an[MI];
-#pragma unroll
-      for (int i = 0; i < MI; ++i) an[i] = Vs[(r0 + 8 * i + g) + (size_t)q * b];
       for (int ks = 0; ks < nw / 4; ++ks) {
         double a[MI], bq[SNJ];
 #pragma unroll
@@ -392,8 +393,10 @@ __device__ inline void ssrfb_mirror(const Ctx& cx, const double* V, const double
       }
     }
     TF_LU_T(27);
-    __syncthreads();  // sW (W2) / sT / sR are rewritten by the next block
+    // this warp's mirror rows (every warp finished reading the mirror in the W pass, which
+    // precedes the W2 barriers), then the barrier before sW / sT / sR are rewritten
     if (c0 + ib < b) mirror();
+    __syncthreads();
     TF_LU_T(28);
   }
   slab_store<MI>(acc, A, b);

@@ -422,7 +422,7 @@ __device__ inline int potrf_128(const Ctx& cx, double* A, double* sm) {
 // TRSM, b = 128: X (128 x 128) <- X L^{-T} in shared memory, right-looking over 32-column
 // blocks: row solves of block jb against L's diagonal block, then X(:, jb+32:) -= X(:, jb
 // block) L(jb+32:, jb block)^T by DMMA fragments from shared memory.
-__device__ inline void trsm_128(const Ctx& cx, const double* L, double* X, double* sm) {
+__device__ inline void trsm_128(const Ctx& cx, const double* L, double* X, double* sm, int ldl = 128, int ldx = 128) {
   constexpr int LD = T128_LD;
   const int tid = threadIdx.x, warp = tid >> 5;
   double* Xs = sm;                        // 128 x LD
@@ -430,7 +430,7 @@ __device__ inline void trsm_128(const Ctx& cx, const double* L, double* X, doubl
   double* D = Ls + NB * LD;               // (NB+1) x NB
   for (int e = tid; e < 128 * 64; e += TF_THREADS) {
     const int r = (2 * e) % 128, c = (2 * e) / 128;
-    const double2 v = __ldcg(reinterpret_cast<const double2*>(X + r + (size_t)c * 128));
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(X + r + (size_t)c * ldx));
     Xs[r + c * LD] = v.x;
     Xs[r + 1 + c * LD] = v.y;
   }
@@ -438,7 +438,7 @@ __device__ inline void trsm_128(const Ctx& cx, const double* L, double* X, doubl
     const int rows = 128 - jb;  // L rows jb .. 127 of the block's columns
     for (int e = tid; e < rows * NB; e += TF_THREADS) {
       const int r = e % rows, c = e / rows;
-      Ls[r + c * LD] = ldg_cg(L + (jb + r) + (size_t)(jb + c) * 128);
+      Ls[r + c * LD] = ldg_cg(L + (jb + r) + (size_t)(jb + c) * ldl);
     }
     __syncthreads();
     for (int e = tid; e < NB * NB; e += TF_THREADS) {
@@ -460,7 +460,7 @@ __device__ inline void trsm_128(const Ctx& cx, const double* L, double* X, doubl
   }
   for (int e = tid; e < 128 * 64; e += TF_THREADS) {
     const int r = (2 * e) % 128, c = (2 * e) / 128;
-    *reinterpret_cast<double2*>(X + r + (size_t)c * 128) = make_double2(Xs[r + c * LD], Xs[r + 1 + c * LD]);
+    *reinterpret_cast<double2*>(X + r + (size_t)c * ldx) = make_double2(Xs[r + c * LD], Xs[r + 1 + c * LD]);
   }
 }
 
@@ -497,18 +497,38 @@ __device__ inline void trsm_right(const Ctx& cx, const double* L, double* X, int
   const int r0 = item * RB, rows = min(RB, b - r0);
   double* D = sm + GemmNT32::SMEM_DOUBLES;
   X += r0;
-  for (int J = 0; J < b; J += 128) {
-    for (int jb = J; jb < J + 128; jb += NB) {
-      if (jb > J) {
-        GemmNT32 g;
+  if (rows == 128) {
+    // left-looking over 128-column panels: X(:, J:J+128) -= X(:, 0:J) L(J:J+128, 0:J)^T as ONE
+    // DMMA-engine product with K = J (fewer, longer pipelines than a rank-128 update per panel
+    // pair), then the panel's 128 x 128 block solved entirely in shared memory (trsm_128)
+    for (int J = 0; J < b; J += 128) {
+      if (J > 0) {
+        GemmNT128 g;
         g.zero();
-        g.run(sm, X + (size_t)J * b, b, L + jb + (size_t)J * b, b, rows, NB, jb - J);
-        sub_store(g, X + (size_t)jb * b, b, rows, NB);
+        g.run(sm, X, b, L + J, b, rows, 128, J);
+        sub_store(g, X + (size_t)J * b, b, rows, 128);
+        __syncthreads();
       }
-      load_lower_block(D, L + jb + (size_t)jb * b, b, NB);  // (has __syncthreads)
-      row_solve(X + (size_t)jb * b, b, rows, NB, D);
+      trsm_128(cx, L + J + (size_t)J * b, X + (size_t)J * b, sm, b, b);
       fence_proxy_async_all();
       __syncthreads();
+    }
+    return;
+  }
+  for (int J = 0; J < b; J += 128) {
+    {
+      for (int jb = J; jb < J + 128; jb += NB) {
+        if (jb > J) {
+          GemmNT32 g;
+          g.zero();
+          g.run(sm, X + (size_t)J * b, b, L + jb + (size_t)J * b, b, rows, NB, jb - J);
+          sub_store(g, X + (size_t)jb * b, b, rows, NB);
+        }
+        load_lower_block(D, L + jb + (size_t)jb * b, b, NB);  // (has __syncthreads)
+        row_solve(X + (size_t)jb * b, b, rows, NB, D);
+        fence_proxy_async_all();
+        __syncthreads();
+      }
     }
     // columns to the right: X(:, n0:n0+128) -= X(:, J:J+128) L(n0:n0+128, J:J+128)^T
     for (int n0 = J + 128; n0 < b; n0 += 128) {

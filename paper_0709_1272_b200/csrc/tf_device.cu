@@ -348,6 +348,7 @@ __device__ inline void run_item(const Prob& P, const Sched& S, const Dist& D, co
     // slab-level DAG panel tasks (d.pad = slab)
     case K_GEQRT_S: geqrt_slab_item(cx, a.T(k, k), a.STRIP(k, k), a.VX(k), d.pad, sm); break;
     case K_TSQRT_S: tsqrt_slab_item(cx, a.T(k, k), a.T(i, k), a.STRIP(i, k), d.pad, sm); break;
+    case K_TSTRF_A: tstrf_apply_item(cx, a.T(k, k), a.T(i, k), a.STRIP(i, k), a.PIV(i, k), d.pad, sm); break;
     case K_GETRF_S: {
       const int f = getrf_slab_item(cx, a.T(k, k), a.PIV(k, k), a.VX(k), d.pad, sm);
       if (f >= 0 && threadIdx.x == 0) atomicMin(cx.info, k * P.b + f + 1);

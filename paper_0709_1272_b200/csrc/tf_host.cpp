@@ -175,6 +175,10 @@ void global_tasks_fine(int alg, int p, int b, int ib, int policy, std::vector<Ta
   const int S = b / NSR;
   const int F = alg == 1 ? 4 : 8, R = F + 1, C = F + 2, U = F + 3;
   const int FS = alg == 1 ? K_GEQRT_S : K_GETRF_S, CS = alg == 1 ? K_TSQRT_S : K_TSTRF_S;
+  const int CA = alg == 1 ? K_TSQRT_A : K_TSTRF_A;
+  // finished inner blocks before slab s; the last slab of inner block t
+  auto nfull = [&](int s) { return (s * NSR - (s * NSR) % ib) / ib; };
+  auto last_slab = [&](int t) { return (t + 1) * ib / NSR - 1; };
   std::unordered_map<uint64_t, int> id;
   tasks.clear();
   // split (per-slab) tasks: key kind | 32, j' = j * 64 + s
@@ -195,7 +199,10 @@ void global_tasks_fine(int alg, int p, int b, int ib, int policy, std::vector<Ta
       else add(R, k, k, j, -1, nit);
     }
     for (int i = k + 1; i < p; ++i) {
-      for (int s = 0; s < S; ++s) add(CS, k, i, k, s, 1);
+      for (int s = 0; s < S; ++s) {
+        if (ts_apply_split(alg == 2) && nfull(s) >= 2) add(CA, k, i, k, s, 1);  // older inner blocks, off the chain
+        add(CS, k, i, k, s, 1);
+      }
       for (int j = k + 1; j < qc; ++j) {
         if (j == k + 1) for (int s = 0; s < nit; ++s) add(U, k, i, j, s, 1);
         else add(U, k, i, j, -1, nit);
@@ -219,10 +226,22 @@ void global_tasks_fine(int alg, int p, int b, int ib, int policy, std::vector<Ta
     if (d.kind == FS) {
       if (s > 0) P(get(FS, k, k, k, s - 1));
       if (k > 0) P(upd(U, k - 1, k, k, s));
-    } else if (d.kind == CS) {
-      if (s > 0) P(get(CS, k, i, k, s - 1));
+    } else if (d.kind == CA) {
+      // inner blocks [0, nfull(s) - 1) of TSQRT / TSTRF (i,k) applied to slab s: after block
+      // nfull(s) - 2 is factored, the previous TSQRT / TSTRF of the column left slab s of the
+      // diagonal tile, and step k-1 updated slab s of tile (i,k)
+      P(get(CS, k, i, k, last_slab(nfull(s) - 2)));
       P(i == k + 1 ? get(FS, k, k, k, s) : get(CS, k, i - 1, k, s));
       if (k > 0) P(upd(U, k - 1, i, k, s));
+    } else if (d.kind == CS) {
+      if (s > 0) P(get(CS, k, i, k, s - 1));
+      const int ca = get(CA, k, i, k, s);
+      if (ca >= 0) {
+        P(ca);
+      } else {
+        P(i == k + 1 ? get(FS, k, k, k, s) : get(CS, k, i - 1, k, s));
+        if (k > 0) P(upd(U, k - 1, i, k, s));
+      }
     } else if (d.kind == R) {
       P(get(FS, k, k, k, S - 1));
       if (k > 0) P(upd(U, k - 1, k, j, split ? s : -1));

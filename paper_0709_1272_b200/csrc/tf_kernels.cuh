@@ -950,7 +950,7 @@ __device__ inline void tsqrt_item(const Ctx& cx, double* R, double* A, double* T
   if (ssrfb_reg_ok(cx.b, cx.ib)) TF_SLAB_DISPATCH(v_qr_slab, cx, true, A, R, Tst, nullptr, 0, cx.b);
   else v_tsqrt_ref(cx, R, A, Tst);
 }
-// TSQRT slab task of the slab-level DAG: 32-column slab s of [R_kk; A_ik].
+// Slab-level DAG, TSQRT slab s of [R_kk; A_ik].
 __device__ inline void tsqrt_slab_item(const Ctx& cx, double* R, double* A, double* Tst, int s, double* sm) {
   TF_SLAB_DISPATCH(v_qr_slab, cx, true, A, R, Tst, nullptr, s * NSR, (s + 1) * NSR);
 }
@@ -1286,8 +1286,9 @@ TF_DEF_VARIANT(v_ssssm_reg, ssssm_reg,
                (cx, L, Ls, ipiv, U, A, item, dsm))
 TF_DEF_VARIANT_RET(v_getrf_slab, getrf_slab, (Ctx cx, double* A, int* ipiv, double* LX, int cb, int ce),
                    (cx, A, ipiv, LX, cb, ce, dsm))
-TF_DEF_VARIANT_RET(v_tstrf_slab, tstrf_slab, (Ctx cx, double* U, double* A, double* Ls, int* ipiv, int cb, int ce),
-                   (cx, U, A, Ls, ipiv, cb, ce, dsm))
+TF_DEF_VARIANT_RET(v_tstrf_slab, tstrf_slab,
+                   (Ctx cx, double* U, double* A, double* Ls, int* ipiv, int cb, int ce, int bl, int bh, bool pnl),
+                   (cx, U, A, Ls, ipiv, cb, ce, dsm, bl, bh, pnl))
 TF_DEF_REF(v_gessm_ref, gessm_ref, (Ctx cx, const double* LX, const int* ipiv, double* C, int item),
            (cx, LX, ipiv, C, item, dsm))
 TF_DEF_REF(v_ssssm_ref, ssssm_ref,
@@ -1327,12 +1328,21 @@ TF_DEF_REF(v_ungessm, ungessm_item, (Ctx cx, const double* F, const int* ipiv, d
            (cx, F, ipiv, X, item, dsm))
 
 __device__ inline int tstrf_item(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, double* sm) {
-  if (ssrfb_reg_ok(cx.b, cx.ib)) return TF_SLAB_RET(v_tstrf_slab, cx, U, A, Ls, ipiv, 0, cx.b);
+  if (ssrfb_reg_ok(cx.b, cx.ib)) return TF_SLAB_RET(v_tstrf_slab, cx, U, A, Ls, ipiv, 0, cx.b, 0, INT_MAX, true);
   return v_tstrf_ref(cx, U, A, Ls, ipiv);
 }
-// TSTRF slab task of the slab-level DAG.
+// TSTRF slab / apply tasks of the slab-level DAG: the older finished inner blocks [0, nfull - 1)
+// by the apply task, the last one (and for ib = 64 the block's first slab) plus the panel by
+// the slab task (nfull = finished inner blocks before slab s).
+__device__ __forceinline__ int ts_nfull(int s, int ib) { return (s * NSR - (s * NSR) % ib) / ib; }
 __device__ inline int tstrf_slab_item(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, int s, double* sm) {
-  return TF_SLAB_RET(v_tstrf_slab, cx, U, A, Ls, ipiv, s * NSR, (s + 1) * NSR);
+  const int nf = ts_nfull(s, cx.ib);
+  const int lo = ts_apply_split(true) && nf >= 2 ? nf - 1 : 0;
+  return TF_SLAB_RET(v_tstrf_slab, cx, U, A, Ls, ipiv, s * NSR, (s + 1) * NSR, lo, INT_MAX, true);
+}
+__device__ inline void tstrf_apply_item(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, int s, double* sm) {
+  const int nf = ts_nfull(s, cx.ib);
+  (void)TF_SLAB_RET(v_tstrf_slab, cx, U, A, Ls, ipiv, s * NSR, (s + 1) * NSR, 0, nf - 1, false);
 }
 
 }  // namespace tf

@@ -574,8 +574,9 @@ __device__ inline int lu_panel(double* P, int ldp, int cs, int b, double* UL, in
 // ipiv: pivots (i,k).  Returns the first zero-pivot local column or -1.
 template <int MI>
 // Slabs [c_begin, c_end) only (the slab-level DAG's TSTRF slab tasks).
+// blk_lo / blk_hi / panel: as qr_slab (the slab-level graph's TSTRF apply tasks).
 __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls, int* ipiv, int c_begin, int c_end,
-                                 double* sm) {
+                                 double* sm, int blk_lo = 0, int blk_hi = INT_MAX, bool panel = true) {
   const int b = cx.b, ib = cx.ib;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, q = lane & 3;
   constexpr int RW = 8 * MI;
@@ -591,17 +592,24 @@ __device__ inline int tstrf_slab(const Ctx& cx, double* U, double* A, double* Ls
       // the finished inner blocks, then (second slab of a 64-block) the block's first slab
       // as a 32-column sub-block; each block's inputs prefetched during the previous one
       int buf = 0;
-      const int nfull = s0 / ib, nblk = nfull + (off ? 1 : 0);
+      const int nfull = s0 / ib;
+      const int xlo = blk_lo < nfull ? blk_lo : nfull;
+      const int xhi = panel ? nfull + (off ? 1 : 0) : (blk_hi < nfull ? blk_hi : nfull);
       auto blk = [&](int x) {
         const int c0 = x < nfull ? x * ib : s0;
         return LuBlk{U + c0 + (size_t)cs * b, Ls + (size_t)c0 * ib, ipiv + c0, x < nfull ? ib : NSR, ib};
       };
-      for (int x = 0; x < nblk; ++x) {
-        const LuBlk cur = blk(x), nxt = blk(x + 1 < nblk ? x + 1 : x);
+      for (int x = xlo; x < xhi; ++x) {
+        const LuBlk cur = blk(x), nxt = blk(x + 1 < xhi ? x + 1 : x);
         const int c0 = x < nfull ? x * ib : s0;
-        buf = lu_ts_apply<MI>(acc, U + c0 + (size_t)cs * b, A + (size_t)c0 * b, cur, b, sm, buf, x > 0,
-                              x + 1 < nblk ? &nxt : nullptr);
+        buf = lu_ts_apply<MI>(acc, U + c0 + (size_t)cs * b, A + (size_t)c0 * b, cur, b, sm, buf, x > xlo,
+                              x + 1 < xhi ? &nxt : nullptr);
       }
+    }
+    if (!panel) {
+      slab_store<MI>(acc, A + (size_t)cs * b, b);
+      __syncthreads();
+      continue;
     }
     TF_LU_T(8);
     double* P = sm;

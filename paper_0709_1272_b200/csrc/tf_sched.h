@@ -47,9 +47,17 @@ constexpr int K_ARRIVE = 23, K_DONE = 24;
 // the next panel column (j = k + 1) as one task per slab item (pad = item offset), so that
 // consecutive TSQRT / TSTRF of a column and the next panel pipeline slab by slab
 // (DESIGN.md §6); the arithmetic of every tile is unchanged.
-constexpr int K_GEQRT_S = 25, K_TSQRT_S = 26, K_GETRF_S = 27, K_TSTRF_S = 28;
+// K_TSQRT_A / K_TSTRF_A: the older inner blocks of a TSQRT / TSTRF slab (pad = slab),
+// applied off the critical path; the slab task then applies only the newest one and
+// factors the slab.
+constexpr int K_GEQRT_S = 25, K_TSQRT_S = 26, K_GETRF_S = 27, K_TSTRF_S = 28, K_TSQRT_A = 29, K_TSTRF_A = 30;
+// Measured: the split shortens config 3 (LU, 10.2 -> 9.8 ms) but lengthens config 2 (QR,
+// 13.0 -> 14.2 ms: the QR slab's panel dominates and the extra hop costs more than the
+// applies it removes from the chain), so only TSTRF is split.
+TF_HD inline bool ts_apply_split(bool lu) { return lu; }
 TF_HD inline int coarse_kind(int kind) {
-  return kind == K_GEQRT_S ? 4 : kind == K_TSQRT_S ? 6 : kind == K_GETRF_S ? 8 : kind == K_TSTRF_S ? 10 : kind;
+  return kind == K_GEQRT_S ? 4 : (kind == K_TSQRT_S || kind == K_TSQRT_A) ? 6 : kind == K_GETRF_S ? 8
+       : (kind == K_TSTRF_S || kind == K_TSTRF_A) ? 10 : kind;
 }
 
 TF_HD inline int ceil_div(int a, int b) { return (a + b - 1) / b; }

@@ -18,7 +18,8 @@ KINDS = {"potrf": 0, "trsm": 1, "syrk": 2, "gemm": 3, "geqrt": 4, "larfb": 5, "t
          "ssrfb": 7, "getrf": 8, "gessm": 9, "tstrf": 10, "ssssm": 11}
 SOLVE_KINDS = {"unitl": 14, "xgessm": 15, "xssssm": 16, "xlarfb": 17, "xssrfb": 18, "xtrsmu": 19, "xgemm": 20,
                "xunssssm": 21, "xungessm": 22}
-SLAB_KINDS = {"geqrt_s": 25, "tsqrt_s": 26, "getrf_s": 27, "tstrf_s": 28}  # slab-level DAG panel tasks
+SLAB_KINDS = {"geqrt_s": 25, "tsqrt_s": 26, "getrf_s": 27, "tstrf_s": 28,  # slab-level DAG panel tasks
+              "tsqrt_a": 29, "tstrf_a": 30}  # ... and their off-chain apply tasks
 KIND_NAMES = {v: k for k, v in KINDS.items()}
 KIND_NAMES.update({v: k for k, v in SLAB_KINDS.items()})
 ALGS = {"chol": 0, "qr": 1, "lu": 2, "getrs": 3, "ormqr": 4, "qrs": 5, "lu_apply_N": 6}

@@ -105,7 +105,9 @@ def main():
         name = tf.KIND_NAMES[int(kid)]
         m = kinds == kid
         nit = int(rec[m, 1].max()) + 1  # items per task of this kind
-        if name.endswith("_s"):  # slab-level panel task: one 32-column slab of the tile
+        if name.endswith("_a"):  # off-chain apply of older inner blocks to one slab
+            fl = 0.0
+        elif name.endswith("_s"):  # slab-level panel task: one 32-column slab of the tile
             fl = item_flops(name[:-2], b, ib, b // 32)
         else:
             fl = item_flops(name, b, ib, max(nit, b // 32) if name in ("larfb", "ssrfb", "gessm", "ssssm") else nit)

@@ -366,7 +366,7 @@ __device__ __forceinline__ void frag_rank32(double* S, int lds, int r, int cc, c
   S[(r + g) + (size_t)(cc + 2 * q + 1) * lds] = c2[1];
 }
 
-__device__ inline int potrf_128(const Ctx& cx, double* A, double* sm) {
+__device__ inline int potrf_128(const Ctx& cx, double* A, double* sm, int lda = 128) {
   constexpr int LD = T128_LD;
   const int tid = threadIdx.x, warp = tid >> 5;
   double* T = sm;                          // 128 x LD
@@ -375,7 +375,7 @@ __device__ inline int potrf_128(const Ctx& cx, double* A, double* sm) {
   TF_LU_T0();
   for (int e = tid; e < 128 * 64; e += TF_THREADS) {  // lower triangle (upper: zeros)
     const int r = (2 * e) % 128, c = (2 * e) / 128;
-    const double2 v = __ldcg(reinterpret_cast<const double2*>(A + r + (size_t)c * 128));
+    const double2 v = __ldcg(reinterpret_cast<const double2*>(A + r + (size_t)c * lda));
     T[r + c * LD] = r >= c ? v.x : 0.0;
     T[r + 1 + c * LD] = r + 1 >= c ? v.y : 0.0;
   }
@@ -414,7 +414,7 @@ __device__ inline int potrf_128(const Ctx& cx, double* A, double* sm) {
   __syncthreads();
   for (int e = tid; e < 128 * 128; e += TF_THREADS) {
     const int r = e % 128, c = e / 128;
-    if (r >= c) A[r + (size_t)c * 128] = T[r + c * LD];
+    if (r >= c) A[r + (size_t)c * lda] = T[r + c * LD];
   }
   return -1;
 }
@@ -487,6 +487,36 @@ __device__ inline void trsm_left(const Ctx& cx, const double* L, double* X, int 
     fence_proxy_async_all();  // the next block's bulk copies read the rows just solved
     __syncthreads();
   }
+}
+
+// POTRF for b a multiple of 128 (>= 256), left-looking over 128-column panels: the panel's
+// rows take the update from all earlier panels as 128 x 128 DMMA-engine products with K = J
+// (one long pipeline per row block), then its diagonal block is factored and the blocks
+// below it solved entirely in shared memory (potrf_128, trsm_128).  Same operations per
+// element as the right-looking form, in a different order (products exact on the pins).
+__device__ inline int potrf_blocked(const Ctx& cx, double* A, double* sm) {
+  const int b = cx.b;
+  for (int J = 0; J < b; J += 128) {
+    if (J > 0) {
+      for (int r0 = J; r0 < b; r0 += 128) {
+        GemmNT128 g;
+        g.zero();
+        g.run(sm, A + r0, b, A + J, b, 128, 128, J);
+        sub_store(g, A + r0 + (size_t)J * b, b, 128, 128, /*lower_mask=*/r0 == J, r0, J);
+      }
+      __syncthreads();
+    }
+    const int f = potrf_128(cx, A + J + (size_t)J * b, sm, b);
+    if (f >= 0) return J + f;
+    fence_proxy_async_all();
+    __syncthreads();
+    for (int r0 = J + 128; r0 < b; r0 += 128) {
+      trsm_128(cx, A + J + (size_t)J * b, A + r0 + (size_t)J * b, sm, b, b);
+      fence_proxy_async_all();
+      __syncthreads();
+    }
+  }
+  return -1;
 }
 
 // TRSM for b a multiple of 128 (>= 256): right-looking over 128-column panels as POTRF —
@@ -614,6 +644,7 @@ TF_DEF_REF_RET(v_potrf_right, potrf_right, (Ctx cx, double* A), (cx, A, dsm))
 TF_DEF_REF(v_trsm_left, trsm_left, (Ctx cx, const double* L, double* X, int item), (cx, L, X, item, dsm))
 TF_DEF_REF(v_trsm_right, trsm_right, (Ctx cx, const double* L, double* X, int item), (cx, L, X, item, dsm))
 TF_DEF_REF_RET(v_potrf_128, potrf_128, (Ctx cx, double* A), (cx, A, dsm))
+TF_DEF_REF_RET(v_potrf_blocked, potrf_blocked, (Ctx cx, double* A), (cx, A, dsm))
 TF_DEF_REF(v_trsm_128, trsm_128, (Ctx cx, const double* L, double* X), (cx, L, X, dsm))
 TF_DEF_REF(v_syrk, syrk_body, (Ctx cx, const double* A, double* C, int item), (cx, A, C, item, dsm))
 TF_DEF_REF(v_gemm, gemm_body, (Ctx cx, const double* A, const double* B, double* C, int item), (cx, A, B, C, item, dsm))
@@ -624,7 +655,11 @@ TF_DEF_REF(v_gemm, gemm_body, (Ctx cx, const double* A, const double* B, double*
 __device__ inline int potrf_item(const Ctx& cx, double* A, double*) {
   if (cx.b == 128) return v_potrf_128(cx, A);
   if (cx.b < 256 || cx.b % 128) return v_potrf_left(cx, A);
+#ifdef TF_POTRF_RIGHT
   return v_potrf_right(cx, A);
+#else
+  return v_potrf_blocked(cx, A);
+#endif
 }
 __device__ inline void trsm_item(const Ctx& cx, const double* L, double* X, int item, double*) {
   if (cx.b == 128) v_trsm_128(cx, L, X);

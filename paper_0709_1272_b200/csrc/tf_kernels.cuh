@@ -489,6 +489,11 @@ __device__ inline void trsm_left(const Ctx& cx, const double* L, double* X, int 
   }
 }
 
+// the 128 x 128 shared-memory kernels on blocks of a larger tile, as separate variants (one
+// register allocation each, like the other tile kernels)
+TF_DEF_REF_RET(v_potrf_128ld, potrf_128, (Ctx cx, double* A, int lda), (cx, A, dsm, lda))
+TF_DEF_REF(v_trsm_128ld, trsm_128, (Ctx cx, const double* L, double* X, int ldl, int ldx), (cx, L, X, dsm, ldl, ldx))
+
 // POTRF for b a multiple of 128 (>= 256), left-looking over 128-column panels: the panel's
 // rows take the update from all earlier panels as 128 x 128 DMMA-engine products with K = J
 // (one long pipeline per row block), then its diagonal block is factored and the blocks
@@ -511,7 +516,7 @@ __device__ inline int potrf_blocked(const Ctx& cx, double* A, double* sm) {
     fence_proxy_async_all();
     __syncthreads();
     for (int r0 = J + 128; r0 < b; r0 += 128) {
-      trsm_128(cx, A + J + (size_t)J * b, A + r0 + (size_t)J * b, sm, b, b);
+      v_trsm_128ld(cx, A + J + (size_t)J * b, A + r0 + (size_t)J * b, b, b);
       fence_proxy_async_all();
       __syncthreads();
     }
@@ -539,7 +544,7 @@ __device__ inline void trsm_right(const Ctx& cx, const double* L, double* X, int
         sub_store(g, X + (size_t)J * b, b, rows, 128);
         __syncthreads();
       }
-      trsm_128(cx, L + J + (size_t)J * b, X + (size_t)J * b, sm, b, b);
+      v_trsm_128ld(cx, L + J + (size_t)J * b, X + (size_t)J * b, b, b);
       fence_proxy_async_all();
       __syncthreads();
     }

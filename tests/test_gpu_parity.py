@@ -45,8 +45,9 @@ def test_pack_unpack_bitwise(m, n, b):
     (64, 64, 16, 4),      # p = 1
     (16, 1, 1, 5),        # b = 1
     (640, 160, 32, 6),
-    (1536, 512, 64, 7),   # config-4 tile shape, p = 3: right-looking POTRF, GEMM strips
+    (1536, 512, 64, 7),   # config-4 tile shape, p = 3: blocked POTRF, GEMM strips
     (1024, 256, 32, 8),
+    (768, 384, 32, 9),    # b = 384: blocked POTRF over three 128-column panels
 ])
 def test_chol_parity(n, b, ib, seed):
     A = tilegen.spd(n, seed)
@@ -69,7 +70,7 @@ def test_chol_parity(n, b, ib, seed):
 
 
 @pytest.mark.parametrize("n,b", [(256, 64), (384, 128), (90, 30),
-                                 (768, 256), (1024, 512)])  # right-looking POTRF, 4-sub-tile GEMM strips
+                                 (768, 256), (1024, 512), (768, 384)])  # blocked POTRF, 4-sub-tile GEMM strips
 def test_chol_exact_pin_bitwise(n, b):
     A, L0 = tilegen.chol_exact(n, n + b)
     G, _, _, gi = gpu_factor("chol", A, b, b // 2)

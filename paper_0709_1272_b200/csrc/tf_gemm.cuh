@@ -296,9 +296,8 @@ struct Gemm {
     main_mb<VEC>(sm, A, lda, B, ldb, M, N, K);
   }
 
-  // run_mb split in two so that a following GEMM's first slices can be in flight while the
-  // caller stores the previous result (gemm_item's two sub-tiles).  prefill issues the first
-  // NST-1 slices; main_mb runs the k loop; the slice counter lives in `pbase` in between.
+  // run_mb in two parts: prefill issues the first NST-1 slices; main_mb runs the k loop; the
+  // slice counter lives in `pbase` in between.
   uint32_t pbase;
   template <int VEC>
   __device__ __forceinline__ void prefill_mb(double* sm, const double* A, int lda, const double* B, int ldb, int M,
@@ -347,20 +346,63 @@ struct Gemm {
     __syncthreads();
     *reinterpret_cast<volatile uint64_t*>(counter) = base + nk;
   }
+  // nprod products sharing A, product x taking the BN operand columns at B + x * BN (Ntot
+  // columns in all), run as ONE continuous slice stream through the cp.async/mbarrier ring:
+  // no CTA barrier between products, and each warp hands its finished accumulators to
+  // epi(x) right after its own last slice of product x (then restarts from zero), so one
+  // warp's epilogue overlaps the other warps' DMMAs and the next product's slices are
+  // already in flight.  Same arithmetic per product as zero() + run() + epi.
+  template <int VEC, class Epi>
+  __device__ __forceinline__ void chain_mb(double* sm, const double* A, int lda, const double* B, int ldb, int nprod,
+                                           int M, int Ntot, int K, Epi&& epi) {
+    uint64_t* full = pipe_bars_c(sm);
+    uint64_t* empty = full + NST;
+    uint64_t* counter = full + 2 * NST;
+    const int nk = (K + KC - 1) / KC;
+    const int T = nk * nprod;
+    const uint32_t base = (uint32_t)*reinterpret_cast<volatile uint64_t*>(counter);
+    __syncthreads();  // earlier shared-memory users of the stage buffers are done
+    auto fill = [&](int t) {
+      const uint32_t g = base + t;
+      const int s = g % NST;
+      const uint32_t use = g / NST;
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      const int x = t / nk, kt = t - x * nk;
+      const int nn = min(BN, Ntot - x * BN);
+      load_slice<VEC>(sm, s, A, lda, B + (size_t)x * BN, ldb, M, nn, K, kt);
+      cp_async_mbar_arrive(&full[s]);
+    };
+    for (int t = 0; t < NST - 1 && t < T; ++t) fill(t);
+    const int lane = threadIdx.x & 31;
+    zero();
+    int kt = 0, x = 0;
+    for (int t = 0; t < T; ++t) {
+      const uint32_t g = base + t;
+      const int s = g % NST;
+      mbar_wait(&full[s], (g / NST) & 1);
+      compute_slice(sm, s);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (t + NST - 1 < T) fill(t + NST - 1);
+      if (++kt == nk) {
+        epi(x);
+        zero();
+        kt = 0;
+        ++x;
+      }
+    }
+    __syncthreads();
+    *reinterpret_cast<volatile uint64_t*>(counter) = base + T;
+  }
+  template <class Epi>
+  __device__ __forceinline__ void chain(double* sm, const double* A, int lda, const double* B, int ldb, int nprod,
+                                        int M, int Ntot, int K, Epi&& epi) {
+    if (vec2_ok(A, lda, B, ldb)) chain_mb<2>(sm, A, lda, B, ldb, nprod, M, Ntot, K, epi);
+    else chain_mb<1>(sm, A, lda, B, ldb, nprod, M, Ntot, K, epi);
+  }
   __device__ __forceinline__ static bool vec2_ok(const double* A, int lda, const double* B, int ldb) {
     return ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 && ((lda | ldb) & 1) == 0;
   }
-  __device__ __forceinline__ void prefill(double* sm, const double* A, int lda, const double* B, int ldb, int M,
-                                          int N, int K) {
-    if (vec2_ok(A, lda, B, ldb)) prefill_mb<2>(sm, A, lda, B, ldb, M, N, K);
-    else prefill_mb<1>(sm, A, lda, B, ldb, M, N, K);
-  }
-  __device__ __forceinline__ void finish(double* sm, const double* A, int lda, const double* B, int ldb, int M,
-                                         int N, int K) {
-    if (vec2_ok(A, lda, B, ldb)) main_mb<2>(sm, A, lda, B, ldb, M, N, K);
-    else main_mb<1>(sm, A, lda, B, ldb, M, N, K);
-  }
-
   // Full-tile fast path for m/n-contiguous operands: one elected producer thread streams
   // each k-slice with bulk async copies (one per operand column, BM*8 / BN*8 bytes) into the
   // padded stage buffers and signals a per-stage "full" mbarrier by transaction bytes;

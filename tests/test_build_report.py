@@ -16,7 +16,7 @@ LOG = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), 
 BUDGET = {
     "v_qr_slabILi1E": 0, "v_qr_slabILi2E": 0,          # GEQRT / TSQRT, configs 2-3 and b = 128
     "v_ssrfb_mirrorILi2E": 0, "v_larfb_regILi2E": 0,   # config 2 updates
-    "v_gemmENS_3Ctx": 64, "v_syrkENS_3Ctx": 64,        # config 4 (a few bytes of spilled indices)
+    "v_gemmENS_3Ctx": 96, "v_syrkENS_3Ctx": 64,        # config 4 (a few bytes of spilled indices)
     "v_ssrfb_mirrorILi4E": 128,                        # config 5
 }
 

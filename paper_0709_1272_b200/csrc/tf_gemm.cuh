@@ -349,9 +349,10 @@ struct Gemm {
   // nprod products sharing A, product x taking the BN operand columns at B + x * BN (Ntot
   // columns in all), run as ONE continuous slice stream through the cp.async/mbarrier ring:
   // no CTA barrier between products, and each warp hands its finished accumulators to
-  // epi(x) right after its own last slice of product x (then restarts from zero), so one
-  // warp's epilogue overlaps the other warps' DMMAs and the next product's slices are
-  // already in flight.  Same arithmetic per product as zero() + run() + epi.
+  // epi(x) right after its own last slice of product x, so one warp's epilogue overlaps the
+  // other warps' DMMAs and the next product's slices are already in flight.  epi(x) also
+  // sets up the accumulators of product x + 1 (x = -1: of product 0, called once the first
+  // slices are requested): zero() or load_acc().  Same arithmetic per product as run().
   template <int VEC, class Epi>
   __device__ __forceinline__ void chain_mb(double* sm, const double* A, int lda, const double* B, int ldb, int nprod,
                                            int M, int Ntot, int K, Epi&& epi) {
@@ -374,7 +375,7 @@ struct Gemm {
     };
     for (int t = 0; t < NST - 1 && t < T; ++t) fill(t);
     const int lane = threadIdx.x & 31;
-    zero();
+    epi(-1);
     int kt = 0, x = 0;
     for (int t = 0; t < T; ++t) {
       const uint32_t g = base + t;
@@ -386,7 +387,6 @@ struct Gemm {
       if (t + NST - 1 < T) fill(t + NST - 1);
       if (++kt == nk) {
         epi(x);
-        zero();
         kt = 0;
         ++x;
       }

@@ -138,40 +138,40 @@ __device__ inline void load_ts(double* sT, const double* Tst, int ib, int c0) {
 // Cholesky (C1)
 // ====================================================================================
 
-// In-place Cholesky of the nb x nb lower block D (smem, ld NB+1) by warp 0, left-looking
-// per column as in DPOTF2.  Returns -1 or the failing local column.
-// nb = NB: fully unrolled, lane i keeps its row in registers, row j's finished values come
-// as shared-memory broadcasts (independent loads, issued as soon as column j-1 is stored),
-// four interleaved partial sums, no early exit and no divergent branches (one predicated
-// store per column): 262 cycles per column against 454 with an exit test and two branches
-// (tools/chol_bench.cu).
-// (A register-resident right-looking variant with the multipliers by shuffles was measured
-// slower: 496 shuffles issue from one warp; potrf b=128 63 -> 136 us.)
+// In-place Cholesky of the nb x nb lower block D (smem, ld NB+1) by warp 0 (DPOTF2,
+// PAPER.md:260-267).  Returns -1 or the failing local column.
+// nb = NB: right-looking, fully unrolled; lane i keeps row i in registers.  After column j
+// every lane applies the rank-1 update x_i[c] -= L[i][j] L[c][j] (c > j) with L[c][j] read
+// back from shared memory (broadcast loads), while lane j+1 forms the next pivot
+// x_{j+1}[j+1] - L[j+1][j]^2 at once and shuffles it: the per-column critical path is one
+// shuffle, one rsqrt, one multiply and one FMA (175 cycles per column against 262 for the
+// left-looking form with four partial sums, tools/chol_bench.cu).  The subtractions of each
+// element happen in the same order (m = 0, 1, ..., j-1) as the oracle's DPOTF2 dot products.
+// No early exit and no divergent branches: the first failing column is recorded.
+// (A register-resident variant with the multipliers by shuffles was measured slower: 496
+// shuffles issue from one warp; potrf b=128 63 -> 136 us.)
 __device__ inline int chol_diag_block(double* D, int nb, int* sflag) {
   if (nb == NB) {
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
       double x[NB];
 #pragma unroll
-      for (int c = 0; c < NB; ++c) x[c] = c <= lane ? D[lane + c * (NB + 1)] : 0.0;
+      for (int c = 0; c < NB; ++c) x[c] = D[lane + c * (NB + 1)];
       int fail = -1;
+      double d = __shfl_sync(0xffffffffu, x[0], 0);
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        double p[4] = {x[j], 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int m = 0; m < j; ++m) p[m & 3] -= x[m] * D[j + m * (NB + 1)];
-        const double sj = (p[0] + p[1]) + (p[2] + p[3]);
-        const double d = __shfl_sync(0xffffffffu, sj, j);
-        // no early exit: the first failing column is recorded and the caller discards D
         if (!(d > 0.0) && fail < 0) fail = j;
         const double r = rsqrt(d);
-        const double v = (lane == j ? d : sj) * r;  // L_jj = d / sqrt(d), L_rj = s / sqrt(d)
-        if (lane >= j) {
-          x[j] = v;
-          D[lane + j * (NB + 1)] = v;
-        }
+        const double l = (lane == j ? d : x[j]) * r;  // L_jj = d / sqrt(d), L_ij = x_i[j] / sqrt(d)
+        if (lane >= j) D[lane + j * (NB + 1)] = l;
         if (lane == j) D[NB + j * (NB + 1)] = r;  // padding row: reciprocal of L_jj for row_solve
-        __syncwarp();
+        if (j + 1 < NB) {
+          d = __shfl_sync(0xffffffffu, x[j + 1] - l * l, j + 1);
+          __syncwarp();
+#pragma unroll
+          for (int c = j + 1; c < NB; ++c) x[c] -= l * D[c + j * (NB + 1)];
+        }
       }
       if (lane == 0) *sflag = fail;
     }
@@ -428,6 +428,7 @@ __device__ inline void trsm_128(const Ctx& cx, const double* L, double* X, doubl
   double* Xs = sm;                        // 128 x LD
   double* Ls = Xs + 128 * LD;             // L(jb.., jb block): 32 columns, ld LD
   double* D = Ls + NB * LD;               // (NB+1) x NB
+  TF_LU_T0();
   for (int e = tid; e < 128 * 64; e += TF_THREADS) {
     const int r = (2 * e) % 128, c = (2 * e) / 128;
     const double2 v = __ldcg(reinterpret_cast<const double2*>(X + r + (size_t)c * ldx));
@@ -448,8 +449,10 @@ __device__ inline void trsm_128(const Ctx& cx, const double* L, double* X, doubl
       if (r == c) D[NB + c * (NB + 1)] = 1.0 / v;
     }
     __syncthreads();
+    TF_LU_T(4);
     row_solve_smem(Xs + jb * LD, LD, 128, D);
     __syncthreads();
+    TF_LU_T(5);
     const int n0 = jb + NB, ncol = 128 - n0;
     const int nfrag = 16 * (ncol / 8);
     for (int f = warp; f < nfrag; f += TF_WARPS) {
@@ -457,11 +460,13 @@ __device__ inline void trsm_128(const Ctx& cx, const double* L, double* X, doubl
       frag_rank32(Xs, LD, 8 * bi, n0 + 8 * bj, Xs + jb * LD, LD, Ls - jb, LD);  // L(row, jb + k) = Ls[row - jb + k LD]
     }
     __syncthreads();
+    TF_LU_T(6);
   }
   for (int e = tid; e < 128 * 64; e += TF_THREADS) {
     const int r = (2 * e) % 128, c = (2 * e) / 128;
     *reinterpret_cast<double2*>(X + r + (size_t)c * ldx) = make_double2(Xs[r + c * LD], Xs[r + 1 + c * LD]);
   }
+  TF_LU_T(7);
 }
 
 // TRSM (DTRSM): rows [item*RB, +RB) of X <- X L^{-T}, left-looking over
@@ -607,17 +612,20 @@ __device__ inline void gemm_body(const Ctx& cx, const double* A, const double* B
       const int n = (nj * gs + x) * RB;
       prefetch_l2(C + m0 + (size_t)n * b, b, mm, min(RB, b - n));
     }
-    GemmNT128 g;
     const int n0 = nj * gs * RB;
+    GemmNT128 g;
     g.chain(sm, A + m0, b, B + n0, b, gs, mm, min(gs * RB, b - n0), b, [&](int x) {
+      if (x >= 0) {
 #ifndef TF_KB_NOEPI
-      const int n = n0 + x * RB;
-      sub_store(g, C + m0 + (size_t)n * b, b, mm, min(RB, b - n), false, 0, 0, /*red=*/true);
+        const int n = n0 + x * RB;
+        sub_store(g, C + m0 + (size_t)n * b, b, mm, min(RB, b - n), false, 0, 0, /*red=*/true);
 #else
-      double s = 0.0;  // kbench probe only: keep the products live without an epilogue
-      g.for_each(mm, RB, [&](int, int, double v) { s += v; });
-      if (s == 1234.5) C[threadIdx.x] = s;
+        double s = 0.0;  // kbench probe only: keep the products live without an epilogue
+        g.for_each(mm, RB, [&](int, int, double v) { s += v; });
+        if (s == 1234.5) C[threadIdx.x] = s;
 #endif
+      }
+      g.zero();
     });
     return;
   }

@@ -67,6 +67,39 @@ __device__ inline int chol_v2(double* D, int* sflag) {
   return *sflag;
 }
 
+
+// v3: right-looking; lane i holds row i; after column j every lane applies the rank-1 update
+// to its remaining entries with L[c][j] read back from shared memory (broadcast loads), and
+// the next pivot d_{j+1} = x_{j+1}[j+1] - L[j+1][j]^2 is formed by lane j+1 and shuffled
+// (the critical path per column: shuffle, rsqrt, one multiply, one FMA)
+__device__ inline int chol_v3(double* D, int* sflag) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double x[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) x[c] = D[lane + c * (NB + 1)];
+    int fail = -1;
+    double d = __shfl_sync(0xffffffffu, x[0], 0);
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      if (!(d > 0.0) && fail < 0) fail = j;
+      const double r = rsqrt(d);
+      const double l = (lane == j ? d : x[j]) * r;
+      if (lane >= j) D[lane + j * (NB + 1)] = l;
+      if (lane == j) D[NB + j * (NB + 1)] = r;
+      if (j + 1 < NB) {
+        d = __shfl_sync(0xffffffffu, x[j + 1] - l * l, j + 1);
+        __syncwarp();
+#pragma unroll
+        for (int c = j + 1; c < NB; ++c) x[c] -= l * D[c + j * (NB + 1)];
+      }
+    }
+    if (lane == 0) *sflag = fail;
+  }
+  __syncthreads();
+  return *sflag;
+}
+
 template <int V>
 __global__ void __launch_bounds__(TF_THREADS, 1) k(double* out, long long* cyc, int reps) {
   __shared__ double D[(NB + 1) * NB];
@@ -79,22 +112,31 @@ __global__ void __launch_bounds__(TF_THREADS, 1) k(double* out, long long* cyc, 
     }
     __syncthreads();
     const long long t0 = clock64();
-    const int f = V == 0 ? chol_diag_block(D, NB, &sflag) : V == 1 ? chol_v1(D, &sflag) : chol_v2(D, &sflag);
+    const int f = V == 0 ? chol_diag_block(D, NB, &sflag) : V == 1 ? chol_v1(D, &sflag) : V == 2 ? chol_v2(D, &sflag) : chol_v3(D, &sflag);
     const long long t1 = clock64();
     tot += t1 - t0;
     if (f >= 0 && threadIdx.x == 0) out[1] = f;
   }
-  if (threadIdx.x == 0) { cyc[V] = tot; out[0] = D[NB * (NB + 1) - 2]; }
+  if (threadIdx.x == 0) cyc[V] = tot;
+  for (int e = threadIdx.x; e < NB * (NB + 1); e += TF_THREADS) out[8 + V * NB * (NB + 1) + e] = D[e];
 }
 int main() {
   double* o; long long* c;
-  cudaMalloc(&o, 64); cudaMallocManaged(&c, 64);
+  cudaMallocManaged(&o, 8 * (8 + 4 * NB * (NB + 1))); cudaMallocManaged(&c, 64);
   const int reps = 50;
   for (int it = 0; it < 2; ++it) {
     k<0><<<1, TF_THREADS>>>(o, c, reps); k<1><<<1, TF_THREADS>>>(o, c, reps); k<2><<<1, TF_THREADS>>>(o, c, reps);
+    k<3><<<1, TF_THREADS>>>(o, c, reps);
     cudaDeviceSynchronize();
   }
   printf("chol_diag_block: %.0f cycles/column; v1 (row via shuffles): %.0f; v2 (no exit, predicated): %.0f\n",
          c[0] / (double)reps / NB, c[1] / (double)reps / NB, c[2] / (double)reps / NB);
+  double md = 0, mref = 0;
+  for (int j = 0; j < NB; ++j)
+    for (int i = j; i <= NB; ++i) {  // lower triangle and the reciprocal padding row
+      const double a = o[8 + i + j * (NB + 1)], b = o[8 + 3 * NB * (NB + 1) + i + j * (NB + 1)];
+      md = fmax(md, fabs(a - b)); mref = fmax(mref, fabs(a));
+    }
+  printf("v3 (right-looking): %.0f cycles/column; max |v3 - v0| = %.3g (max |v0| %.3g)\n", c[3] / (double)reps / NB, md, mref);
   return 0;
 }

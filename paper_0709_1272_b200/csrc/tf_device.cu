@@ -345,6 +345,16 @@ __device__ inline void run_item(const Prob& P, const Sched& S, const Dist& D, co
       if (f >= 0 && threadIdx.x == 0) atomicMin(cx.info, k * P.b + f + 1);
     } break;
     case 11: ssssm_item(cx, a.T(i, k), a.STRIP(i, k), a.PIV(i, k), a.T(k, j), a.T(i, j), sub + d.pad, sm); break;
+    // panel-level Cholesky DAG (d.pad = 128-column panel)
+    case K_POTRF_D: {
+      const int f = v_potrf_pd(cx, a.T(k, k), d.pad);
+      if (f >= 0 && threadIdx.x == 0) {
+        atomicMin(cx.info, k * P.b + f + 1);
+        atomicExch(cx.abort_flag, 1);
+      }
+    } break;
+    case K_POTRF_B: v_potrf_pb(cx, a.T(k, k), d.pad, sub); break;
+    case K_TRSM_P: v_trsm_p(cx, a.T(k, k), a.T(i, k), d.pad, sub); break;
     // slab-level DAG panel tasks (d.pad = slab)
     case K_GEQRT_S: geqrt_slab_item(cx, a.T(k, k), a.STRIP(k, k), a.VX(k), d.pad, sm); break;
     case K_TSQRT_S: tsqrt_slab_item(cx, a.T(k, k), a.T(i, k), a.STRIP(i, k), d.pad, sm); break;

@@ -254,6 +254,72 @@ void global_tasks_fine(int alg, int p, int b, int ib, int policy, std::vector<Ta
   }
 }
 
+// Panel-level DAG of Algorithm 1 (Cholesky, b a multiple of 128 and >= 256, single GPU).
+// POTRF(k) and TRSM(k,i) are left-looking over nr = b / 128 column panels (potrf_blocked,
+// trsm_right): panel J of a row block needs the panels to its left of that row block and of
+// block row J, and the factored diagonal block (J,J).  As tasks:
+//   PD(k,J)   diagonal block of panel J   <- PB(k,J-1)  [J = 0: SYRK(k-1,k,k)]
+//   PB(k,J)   blocks below it (nr-1-J items) <- PD(k,J)
+//   TP(k,i,J) panel J of TRSM(k,i) (nr items)  <- PD(k,J), TP(k,i,J-1)  [J = 0: GEMM(k-1,i,k)]
+//   SYRK(k,i,i) / GEMM(k,i,j) <- TP(k,.,nr-1) as before
+// (PD(k,J) <- PB(k,J-1) <- PD(k,J-1) ... orders every earlier panel of the diagonal tile
+// before it.)  The per-step chain POTRF -> TRSM shrinks from the whole POTRF plus a whole
+// TRSM to 2 nr - 1 block kernels plus one TRSM panel; every element sees the same
+// operations in the same order as in the tile-level DAG (results are bitwise identical).
+void global_tasks_chol_panel(int p, int b, int policy, std::vector<TaskD>& tasks,
+                             std::vector<std::vector<int>>& preds) {
+  const int nr = b / 128;
+  std::unordered_map<uint64_t, int> id;
+  id.reserve((size_t)p * p * p / 2 + 16);
+  tasks.clear();
+  // local kind codes for the key: 0 PD, 1 PB, 2 TP, 3 SYRK, 4 GEMM; panel in the low 3 bits of j
+  auto key = [&](int lk, int k, int i, int j, int J) { return key4(lk, k, i, j * 8 + J); };
+  auto add = [&](int lk, int kind, int k, int i, int j, int J, int nit) {
+    TaskD d{kind, k, i, j, nit, 0, level_of(coarse_kind(kind), k, j, policy), J};
+    id[key(lk, k, i, j, J)] = (int)tasks.size();
+    tasks.push_back(d);
+  };
+  for (int k = 0; k < p; ++k) {
+    for (int J = 0; J < nr; ++J) {
+      add(0, K_POTRF_D, k, k, k, J, 1);
+      if (J + 1 < nr) add(1, K_POTRF_B, k, k, k, J, nr - 1 - J);
+    }
+    for (int i = k + 1; i < p; ++i)
+      for (int J = 0; J < nr; ++J) add(2, K_TRSM_P, k, i, k, J, nr);
+    for (int i = k + 1; i < p; ++i)
+      for (int j = k + 1; j <= i; ++j) add(i == j ? 3 : 4, i == j ? 2 : 3, k, i, j, 0, items_of(i == j ? 2 : 3, b, 0));
+  }
+  auto get = [&](int lk, int k, int i, int j, int J) -> int {
+    auto it = id.find(key(lk, k, i, j, J));
+    return it == id.end() ? -1 : it->second;
+  };
+  const int nt = (int)tasks.size();
+  preds.assign(nt, {});
+  for (int t = 0; t < nt; ++t) {
+    const TaskD& d = tasks[t];
+    auto& pr = preds[t];
+    auto P = [&](int x) { if (x >= 0) pr.push_back(x); };
+    const int k = d.k, i = d.i, j = d.j, J = d.pad;
+    switch (d.kind) {
+      case K_POTRF_D:
+        if (J > 0) P(get(1, k, k, k, J - 1));
+        else if (k > 0) P(get(3, k - 1, k, k, 0));
+        break;
+      case K_POTRF_B: P(get(0, k, k, k, J)); break;
+      case K_TRSM_P:
+        P(get(0, k, k, k, J));
+        if (J > 0) P(get(2, k, i, k, J - 1));
+        else if (k > 0) P(get(4, k - 1, i, k, 0));
+        break;
+      case 2: P(get(2, k, i, k, nr - 1)); if (k > 0) P(get(3, k - 1, i, i, 0)); break;
+      case 3:
+        P(get(2, k, i, k, nr - 1)); P(get(2, k, j, k, nr - 1));
+        if (k > 0) P(get(4, k - 1, i, j, 0));
+        break;
+    }
+  }
+}
+
 // Solve / apply DAGs (NEXT-3) over the right-hand-side tiles X(i,c), c < q.  The factor
 // tiles are read-only inputs, so dependencies come from the X tiles and the explicit
 // unit-lower copies VX(k) only; they are derived generically (read-after-write,
@@ -373,7 +439,7 @@ void add_copy_tasks(int alg, int p, int b, int ib, std::vector<TaskD>& tasks, st
     auto R = [&](int r, int c) { rd[nr][0] = r; rd[nr][1] = c; ++nr; };
     auto W = [&](int r, int c) { wr[nw][0] = r; wr[nw][1] = c; ++nw; };
     if (alg == 0) {
-      switch (d.kind) {
+      switch (kind) {
         case 0: W(k, k); break;
         case 1: R(k, k); W(i, k); break;
         case 2: R(i, k); W(i, i); break;
@@ -408,7 +474,11 @@ void add_copy_tasks(int alg, int p, int b, int ib, std::vector<TaskD>& tasks, st
 bool fine_dag(int alg, int b, int ib) {
   static const int env = getenv("TF_FINE") ? atoi(getenv("TF_FINE")) : 1;
   const int on = g_slab_dag >= 0 ? g_slab_dag : env;
+  if (alg == 0) return on != 0 && chol_panel_ok(b);
   return on != 0 && (alg == 1 || alg == 2) && ssrfb_reg_ok(b, ib);
+}
+bool fine_ok(int alg, int b, int ib) {
+  return alg == 0 ? chol_panel_ok(b) : ((alg == 1 || alg == 2) && ssrfb_reg_ok(b, ib));
 }
 
 // fine: -1 = fine_dag()'s choice, 0 = tile-level, 1 = slab-level where eligible.
@@ -417,8 +487,10 @@ void build_dag(HostDag& G, int alg, int p, int b, int ib, int policy, int q = 0,
   G.alg = alg; G.p = p; G.b = b; G.policy = policy;
   std::vector<std::vector<int>> preds;
   if (alg >= ALG_GETRS) solve_tasks(alg, p, b, ib, q, policy, G.tasks, preds);
-  else if (fine < 0 ? fine_dag(alg, b, ib) : (fine > 0 && (alg == 1 || alg == 2) && ssrfb_reg_ok(b, ib)))
-    global_tasks_fine(alg, p, b, ib, policy, G.tasks, preds, qc);
+  else if (fine < 0 ? fine_dag(alg, b, ib) : (fine > 0 && fine_ok(alg, b, ib))) {
+    if (alg == 0) global_tasks_chol_panel(p, b, policy, G.tasks, preds);
+    else global_tasks_fine(alg, p, b, ib, policy, G.tasks, preds, qc);
+  }
   else global_tasks(alg, p, b, ib, policy, G.tasks, preds, qc);
   if (e2e) add_copy_tasks(alg, p, b, ib, G.tasks, preds);
   finalize_dag(G, preds);
@@ -1275,7 +1347,7 @@ int64_t tile_dag_export(int alg, int64_t p, int policy, int32_t* kind, int32_t* 
 int64_t tile_dag_export_slab(int alg, int64_t p, int64_t b, int64_t ib, int policy, int32_t* kind, int32_t* k,
                              int32_t* i, int32_t* j, int32_t* slab, int32_t* level, int64_t cap, int64_t* succ_off,
                              int32_t* succ, int64_t succ_cap, int64_t* nedges) {
-  if ((alg != 1 && alg != 2) || p <= 0 || !ssrfb_reg_ok((int)b, (int)ib)) return -1;
+  if (alg < 0 || alg > 2 || p <= 0 || !fine_ok(alg, (int)b, (int)ib)) return -1;
   HostDag G;
   build_dag(G, alg, (int)p, (int)b, (int)ib, policy, 0, -1, 0, /*fine=*/1);
   const int64_t nt = (int64_t)G.tasks.size();

@@ -581,6 +581,58 @@ __device__ inline void trsm_right(const Ctx& cx, const double* L, double* X, int
   }
 }
 
+// Panel-level Cholesky DAG (tf_sched.h K_POTRF_D / K_POTRF_B / K_TRSM_P): the bodies of
+// potrf_blocked's and trsm_right's panel loops as separate work items, so every element sees
+// the same operations in the same order as in the one-item kernels (bitwise identical).
+// Diagonal block of panel Jp: update from the panels to its left (K = J), then potrf_128.
+__device__ inline int potrf_panel_diag(const Ctx& cx, double* A, int Jp, double* sm) {
+  const int b = cx.b, J = Jp * 128;
+  if (J > 0) {
+    GemmNT128 g;
+    g.zero();
+    g.run(sm, A + J, b, A + J, b, 128, 128, J);
+    sub_store(g, A + J + (size_t)J * b, b, 128, 128, /*lower_mask=*/true, J, J);
+    __syncthreads();
+  }
+  const int f = potrf_128(cx, A + J + (size_t)J * b, sm, b);
+  fence_proxy_async_all();
+  __syncthreads();
+  return f >= 0 ? J + f : -1;
+}
+// Block row r0 = J + 128 (item + 1) of panel Jp: the same update, then the solve against the
+// factored diagonal block.
+__device__ inline void potrf_panel_below(const Ctx& cx, double* A, int Jp, int item, double* sm) {
+  const int b = cx.b, J = Jp * 128, r0 = J + 128 * (item + 1);
+  if (J > 0) {
+    GemmNT128 g;
+    g.zero();
+    g.run(sm, A + r0, b, A + J, b, 128, 128, J);
+    sub_store(g, A + r0 + (size_t)J * b, b, 128, 128, /*lower_mask=*/false, r0, J);
+    __syncthreads();
+  }
+  v_trsm_128ld(cx, A + J + (size_t)J * b, A + r0 + (size_t)J * b, b, b);
+  fence_proxy_async_all();
+  __syncthreads();
+}
+// Panel Jp of TRSM row block `item` (trsm_right's full-row-block loop body).
+__device__ inline void trsm_panel(const Ctx& cx, const double* L, double* X, int Jp, int item, double* sm) {
+  const int b = cx.b, J = Jp * 128;
+  X += item * RB;
+  if (J > 0) {
+    GemmNT128 g;
+    g.zero();
+    g.run(sm, X, b, L + J, b, 128, 128, J);
+    sub_store(g, X + (size_t)J * b, b, 128, 128);
+    __syncthreads();
+  }
+  v_trsm_128ld(cx, L + J + (size_t)J * b, X + (size_t)J * b, b, b);
+  fence_proxy_async_all();
+  __syncthreads();
+}
+TF_DEF_REF_RET(v_potrf_pd, potrf_panel_diag, (Ctx cx, double* A, int Jp), (cx, A, Jp, dsm))
+TF_DEF_REF(v_potrf_pb, potrf_panel_below, (Ctx cx, double* A, int Jp, int item), (cx, A, Jp, item, dsm))
+TF_DEF_REF(v_trsm_p, trsm_panel, (Ctx cx, const double* L, double* X, int Jp, int item), (cx, L, X, Jp, item, dsm))
+
 // SYRK (DGSMM with i = j): lower sub-tile `item` of C -= A A^T.
 __device__ inline void syrk_body(const Ctx& cx, const double* A, double* C, int item, double* sm) {
   const int b = cx.b;

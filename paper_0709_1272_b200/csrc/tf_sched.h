@@ -55,7 +55,17 @@ constexpr int K_GEQRT_S = 25, K_TSQRT_S = 26, K_GETRF_S = 27, K_TSTRF_S = 28, K_
 // 13.0 -> 14.2 ms: the QR slab's panel dominates and the extra hop costs more than the
 // applies it removes from the chain), so only TSTRF is split.
 TF_HD inline bool ts_apply_split(bool lu) { return lu; }
+// panel-level DAG (Cholesky, b a multiple of 128, >= 256, single GPU): POTRF(k) runs as one
+// task per 128-column panel J (pad = J / 128) for the diagonal block (K_POTRF_D: update from
+// the panels to its left, then the 128 x 128 factorization) and one for the blocks below it
+// (K_POTRF_B: one item per 128-row block, update then triangular solve); TRSM(k,i) as one
+// task per panel (K_TRSM_P, one item per 128-row block), so the TRSMs of a column start
+// after the first diagonal block instead of after the whole POTRF.
+constexpr int K_POTRF_D = 31, K_POTRF_B = 32, K_TRSM_P = 33;
+TF_HD inline bool chol_panel_ok(int b) { return b >= 256 && b % 128 == 0; }
 TF_HD inline int coarse_kind(int kind) {
+  if (kind == K_POTRF_D || kind == K_POTRF_B) return 0;
+  if (kind == K_TRSM_P) return 1;
   return kind == K_GEQRT_S ? 4 : (kind == K_TSQRT_S || kind == K_TSQRT_A) ? 6 : kind == K_GETRF_S ? 8
        : (kind == K_TSTRF_S || kind == K_TSTRF_A) ? 10 : kind;
 }

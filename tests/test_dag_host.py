@@ -514,3 +514,97 @@ def test_slab_dag_shorter_chains():
         w = S * (S + 1) // 2 if int(c["kind"][t]) in (8, 10) else S
         Lc[t] = w + max((Lc[u] for u in prc[t]), default=0)
     assert L.max() < 0.7 * Lc.max(), (L.max(), Lc.max())  # 816 vs 1236 units at p = 16, b = 256
+
+
+# ---------------------------------------------------------------- panel-level Cholesky graph
+def _chol_panel_rw(kind, k, i, j, J, nr):
+    """Read / write regions of the panel-level Cholesky tasks, independent of the builder:
+    every tile is split into 128 x 128 blocks (tile row, tile col, block row, block col).
+    POTRF / TRSM are left-looking over the 128-column panels (PAPER.md:260-274 on blocks):
+    panel J of a block row reads that row's and block row J's panels to the left and the
+    diagonal block (J,J)."""
+    B = lambda r, c, br, bc: (r, c, br, bc)  # noqa: E731
+    left = lambda r, c, br: [B(r, c, br, K_) for K_ in range(J)]  # noqa: E731
+    if kind == 31:  # diagonal block of panel J
+        return left(k, k, J), [B(k, k, J, J)]
+    if kind == 32:  # block rows below it
+        rd, wr = left(k, k, J) + [B(k, k, J, J)], []
+        for r in range(J + 1, nr):
+            rd += left(k, k, r)
+            wr.append(B(k, k, r, J))
+        return rd, wr
+    if kind == 33:  # panel J of TRSM (k, i), every block row
+        rd, wr = left(k, k, J) + [B(k, k, J, J)], []
+        for r in range(nr):
+            rd += left(i, k, r)
+            wr.append(B(i, k, r, J))
+        return rd, wr
+    full = lambda r, c: [B(r, c, br, bc) for br in range(nr) for bc in range(nr)]  # noqa: E731
+    if kind == 2:  # SYRK writes the lower blocks of (i,i)
+        return full(i, k), [B(i, i, br, bc) for br in range(nr) for bc in range(br + 1)]
+    assert kind == 3
+    return full(i, k) + full(j, k), full(i, j)
+
+
+@pytest.mark.parametrize("p,b", [(5, 256), (4, 384), (4, 512), (3, 1024)])
+def test_chol_panel_dag_orders_every_hazard(p, b):
+    """Soundness of the panel-level Cholesky graph: every RAW / WAR / WAW
+    conflict of the independent 128 x 128 block model above is ordered by a path of the
+    exported graph, and the graph has the expected task census."""
+    d = tf.tile_dag_export_slab("chol", p, b, 32)
+    nr = b // 128
+    nt = len(d["kind"])
+    kinds = [int(x) for x in d["kind"]]
+    assert kinds.count(31) == p * nr and kinds.count(32) == p * (nr - 1)
+    assert kinds.count(33) == nr * p * (p - 1) // 2
+    assert kinds.count(2) == p * (p - 1) // 2 and kinds.count(3) == p * (p - 1) * (p - 2) // 6
+    assert kinds.count(0) == kinds.count(1) == 0
+    pr = _preds(d)
+    last_w, readers, hazards = {}, {}, []
+    for t in range(nt):
+        rd, wr = _chol_panel_rw(kinds[t], int(d["k"][t]), int(d["i"][t]), int(d["j"][t]), int(d["slab"][t]), nr)
+        h = set()
+        for r in rd + wr:
+            if r in last_w:
+                h.add(last_w[r])
+        for r in wr:
+            h.update(readers.get(r, ()))
+        h.discard(t)
+        hazards.append(h)
+        for r in rd:
+            readers.setdefault(r, set()).add(t)
+        for r in wr:
+            last_w[r] = t
+            readers[r] = set()
+    anc = [set() for _ in range(nt)]
+    for t in range(nt):
+        for u in pr[t]:
+            assert u < t, "edges follow program order"
+            anc[t] |= anc[u] | {u}
+        missing = hazards[t] - anc[t]
+        assert not missing, (t, kinds[t], int(d["k"][t]), int(d["i"][t]), int(d["j"][t]), int(d["slab"][t]),
+                             [(kinds[u], int(d["k"][u]), int(d["i"][u]), int(d["j"][u]), int(d["slab"][u]))
+                              for u in missing])
+
+
+def test_chol_panel_dag_shorter_chain():
+    """Critical path in units of one 128 x 128 block kernel (a diagonal factorization or a
+    triangular solve, with its update): tile-level POTRF = 2 nr - 1 and TRSM = nr units per
+    step; panel-level the TRSM panels follow the diagonal blocks one by one, so a step costs
+    2 nr - 1 + 1.  SYRK / GEMM items = 1 unit."""
+    p, b = 16, 512
+    nr = b // 128
+    d = tf.tile_dag_export_slab("chol", p, b, 32)
+    pr = _preds(d)
+    L = np.zeros(len(pr))
+    for t in range(len(pr)):
+        L[t] = 1 + max((L[u] for u in pr[t]), default=0)
+    c = tf.tile_dag_export("chol", p)
+    prc = _preds(c)
+    Lc = np.zeros(len(prc))
+    for t in range(len(prc)):
+        w = {0: 2 * nr - 1, 1: nr}.get(int(c["kind"][t]), 1)
+        Lc[t] = w + max((Lc[u] for u in prc[t]), default=0)
+    assert Lc.max() == (p - 1) * (3 * nr) + 2 * nr - 1
+    assert L.max() == (p - 1) * (2 * nr + 1) + 2 * nr - 1
+    assert L.max() < 0.8 * Lc.max()

@@ -28,15 +28,32 @@ def _both(fn):
 @pytest.mark.parametrize("alg,n,b,ib,seed", [("qr", 1024, 256, 32, 0), ("lu", 1024, 256, 32, 1),
                                              ("qr", 1536, 512, 64, 2), ("lu", 1536, 512, 64, 3),
                                              ("qr", 640, 128, 32, 4), ("lu", 640, 128, 64, 5),
-                                             ("lu", 2048, 256, 64, 6)])
+                                             ("lu", 2048, 256, 64, 6),
+                                             # panel-level Cholesky graph (b a multiple of 128, >= 256)
+                                             ("chol", 2048, 512, 64, 7), ("chol", 1280, 256, 32, 8),
+                                             ("chol", 1152, 384, 32, 9), ("chol", 2048, 1024, 64, 10)])
 def test_slab_dag_bitwise_equals_tile_dag(alg, n, b, ib, seed):
-    A = (tilegen.uniform if alg == "qr" else tilegen.normal)(n, seed)
+    A = {"chol": tilegen.spd, "qr": tilegen.uniform, "lu": tilegen.normal}[alg](n, seed)
     (G0, X0, P0, i0), (G1, X1, P1, i1) = _both(lambda: gpu_factor(alg, A, b, ib))
     assert np.array_equal(G0.view(np.int64), G1.view(np.int64))
-    assert np.array_equal(X0.view(np.int64), X1.view(np.int64))
+    if alg != "chol":
+        assert np.array_equal(X0.view(np.int64), X1.view(np.int64))
     if alg == "lu":
         assert np.array_equal(P0, P1)
     assert i0 == i1 == 0
+
+
+@pytest.mark.parametrize("col", [70, 300, 512 + 130, 1023])
+def test_panel_dag_chol_not_spd_info(col):
+    """A non-positive pivot inside a later 128-column panel / tile: info comes from the
+    panel-level diagonal-block task and equals the tile-level graph's and the oracle's."""
+    import oracle
+    n, b = 1024, 512
+    A = tilegen.spd(n, 11)
+    A[col, col] = -1e6
+    (_, _, _, i0), (_, _, _, i1) = _both(lambda: gpu_factor("chol", A, b, 64))
+    F = oracle.pack(A, b)
+    assert i0 == i1 == oracle.chol(F, n, b) == col + 1
 
 
 def test_slab_dag_singular_lu_info():

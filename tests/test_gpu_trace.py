@@ -24,7 +24,8 @@ from paper_0709_1272_b200 import tilefact as tf  # noqa: E402
 @pytest.mark.parametrize("alg,n,b,ib,slab", [("chol", 1024, 128, 32, 0), ("qr", 1024, 256, 32, 1),
                                              ("lu", 1024, 256, 32, 1), ("qr", 1024, 256, 32, 0),
                                              ("lu", 1024, 256, 32, 0), ("lu", 1536, 512, 64, 1),
-                                             ("chol", 2048, 512, 64, 0)])
+                                             ("chol", 2048, 512, 64, 0), ("chol", 2048, 512, 64, 1),
+                                             ("chol", 1536, 256, 32, 1)])
 def test_trace_respects_dag(alg, n, b, ib, slab):
     A = {"chol": tilegen.spd, "qr": tilegen.uniform, "lu": tilegen.normal}[alg](n, 3)
     tf.tile_set_trace(1 << 22)

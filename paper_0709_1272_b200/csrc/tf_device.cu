@@ -330,7 +330,10 @@ __device__ inline void run_item(const Prob& P, const Sched& S, const Dist& D, co
     } break;
     case 1: trsm_item(cx, a.T(k, k), a.T(i, k), sub, sm); break;
     case 2: syrk_item(cx, a.T(i, k), a.T(i, i), sub, sm); break;
-    case 3: gemm_item(cx, a.T(i, k), a.T(j, k), a.T(i, j), sub, sm); break;
+    case 3:
+      if (d.pad) v_gemm_tile(cx, a.T(i, k), a.T(j, k), a.T(i, j));  // whole tile as one item (panel-level graph)
+      else gemm_item(cx, a.T(i, k), a.T(j, k), a.T(i, j), sub, sm);
+      break;
     case 4: geqrt_item(cx, a.T(k, k), a.STRIP(k, k), a.VX(k), sm); break;
     case 5: larfb_item(cx, a.VX(k), a.STRIP(k, k), a.T(k, j), sub + d.pad, sm); break;
     case 6: tsqrt_item(cx, a.T(k, k), a.T(i, k), a.STRIP(i, k), sm); break;

@@ -394,6 +394,52 @@ struct Gemm {
     __syncthreads();
     *reinterpret_cast<volatile uint64_t*>(counter) = base + T;
   }
+  // chain_mb over a grid of full BM x BN products: product x takes the operand rows
+  // A + (x / nper) * BM and columns B + (x % nper) * BN (nper products per A strip), so a
+  // whole tile's sub-tiles run as one slice stream: the pipeline fill, the last epilogue and
+  // the scheduler round trip are paid once per tile instead of once per strip.  A separate
+  // function (not a generalisation of chain_mb) so the strip variant keeps its registers.
+  template <int VEC, class Epi>
+  __device__ __forceinline__ void chain2_mb(double* sm, const double* A, int lda, const double* B, int ldb, int nprod,
+                                            int nper, int K, Epi&& epi) {
+    uint64_t* full = pipe_bars_c(sm);
+    uint64_t* empty = full + NST;
+    uint64_t* counter = full + 2 * NST;
+    const int nk = (K + KC - 1) / KC;
+    const int T = nk * nprod;
+    const uint32_t base = (uint32_t)*reinterpret_cast<volatile uint64_t*>(counter);
+    __syncthreads();  // earlier shared-memory users of the stage buffers are done
+    auto fill = [&](int t) {
+      const uint32_t g = base + t;
+      const int s = g % NST;
+      const uint32_t use = g / NST;
+      if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+      const int x = t / nk, kt = t - x * nk;
+      const int xa = x / nper, xb = x - xa * nper;
+      load_slice<VEC>(sm, s, A + (size_t)xa * BM, lda, B + (size_t)xb * BN, ldb, BM, BN, K, kt);
+      cp_async_mbar_arrive(&full[s]);
+    };
+    for (int t = 0; t < NST - 1 && t < T; ++t) fill(t);
+    const int lane = threadIdx.x & 31;
+    epi(-1);
+    int kt = 0, x = 0;
+    for (int t = 0; t < T; ++t) {
+      const uint32_t g = base + t;
+      const int s = g % NST;
+      mbar_wait(&full[s], (g / NST) & 1);
+      compute_slice(sm, s);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (t + NST - 1 < T) fill(t + NST - 1);
+      if (++kt == nk) {
+        epi(x);
+        kt = 0;
+        ++x;
+      }
+    }
+    __syncthreads();
+    *reinterpret_cast<volatile uint64_t*>(counter) = base + T;
+  }
   template <class Epi>
   __device__ __forceinline__ void chain(double* sm, const double* A, int lda, const double* B, int ldb, int nprod,
                                         int M, int Ntot, int K, Epi&& epi) {

@@ -266,16 +266,28 @@ void global_tasks_fine(int alg, int p, int b, int ib, int policy, std::vector<Ta
 // before it.)  The per-step chain POTRF -> TRSM shrinks from the whole POTRF plus a whole
 // TRSM to 2 nr - 1 block kernels plus one TRSM panel; every element sees the same
 // operations in the same order as in the tile-level DAG (results are bitwise identical).
+// GEMM(k,i,j) outside the lookahead column runs as ONE whole-tile item (pad = 1,
+// gemm_tile_body: the nr x nr sub-tile products as one slice stream) while step k has at
+// least TF_GEMM_TILE_MIN (default 296 = 2 x 148 SMs) such tiles, so the per-item costs
+// (scheduler round trip, pipeline fill, last epilogue) are paid once per tile; later steps
+// and the lookahead column keep the finer strip items for load balance and latency.
+int g_gemm_tile_min = -1;  // tile_set_gemm_tile_min: -1 = default (TF_GEMM_TILE_MIN env, else 296)
+int gemm_tile_min() {
+  static const int env = getenv("TF_GEMM_TILE_MIN") ? atoi(getenv("TF_GEMM_TILE_MIN")) : 296;
+  return g_gemm_tile_min >= 0 ? g_gemm_tile_min : env;
+}
+
 void global_tasks_chol_panel(int p, int b, int policy, std::vector<TaskD>& tasks,
                              std::vector<std::vector<int>>& preds) {
   const int nr = b / 128;
+  const int tile_min = gemm_tile_min();
   std::unordered_map<uint64_t, int> id;
   id.reserve((size_t)p * p * p / 2 + 16);
   tasks.clear();
   // local kind codes for the key: 0 PD, 1 PB, 2 TP, 3 SYRK, 4 GEMM; panel in the low 3 bits of j
   auto key = [&](int lk, int k, int i, int j, int J) { return key4(lk, k, i, j * 8 + J); };
-  auto add = [&](int lk, int kind, int k, int i, int j, int J, int nit) {
-    TaskD d{kind, k, i, j, nit, 0, level_of(coarse_kind(kind), k, j, policy), J};
+  auto add = [&](int lk, int kind, int k, int i, int j, int J, int nit, int pad = -1) {
+    TaskD d{kind, k, i, j, nit, 0, level_of(coarse_kind(kind), k, j, policy), pad >= 0 ? pad : J};
     id[key(lk, k, i, j, J)] = (int)tasks.size();
     tasks.push_back(d);
   };
@@ -286,8 +298,14 @@ void global_tasks_chol_panel(int p, int b, int policy, std::vector<TaskD>& tasks
     }
     for (int i = k + 1; i < p; ++i)
       for (int J = 0; J < nr; ++J) add(2, K_TRSM_P, k, i, k, J, nr);
+    const int m = p - k - 1;
+    const bool whole = tile_min > 0 && (m - 1) * (m - 2) / 2 >= tile_min;  // GEMM tiles with j > k + 1
     for (int i = k + 1; i < p; ++i)
-      for (int j = k + 1; j <= i; ++j) add(i == j ? 3 : 4, i == j ? 2 : 3, k, i, j, 0, items_of(i == j ? 2 : 3, b, 0));
+      for (int j = k + 1; j <= i; ++j) {
+        if (i == j) add(3, 2, k, i, j, 0, items_of(2, b, 0));
+        else if (whole && j > k + 1) add(4, 3, k, i, j, 0, 1, /*pad=*/1);
+        else add(4, 3, k, i, j, 0, items_of(3, b, 0));
+      }
   }
   auto get = [&](int lk, int k, int i, int j, int J) -> int {
     auto it = id.find(key(lk, k, i, j, J));
@@ -653,7 +671,7 @@ void free_dag(DevDag& D) {
 }
 
 int get_dag(int dev, int alg, int p, int b, int ib, DevDag** out, int q = 0, int qc = -1, int e2e = 0) {
-  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy * 4 + (fine_dag(alg, b, ib) ? 2 : 0), q, qc, e2e);
+  auto key = std::make_tuple(dev, alg, p, b, ib, g_policy * 4 + (fine_dag(alg, b, ib) ? 2 : 0) + 8 * (alg == 0 ? gemm_tile_min() : 0), q, qc, e2e);
   auto it = g_dags.find(key);
   if (it != g_dags.end()) { *out = &it->second; return 0; }
   DevDag D;
@@ -1306,6 +1324,7 @@ int tile_factor_host(int kind, int64_t n, int64_t b, int64_t ib, double* hA, dou
 
 void tile_set_policy(int policy) { g_policy = (policy == 0) ? 0 : 1; }
 void tile_set_slab_dag(int on) { g_slab_dag = on < 0 ? -1 : (on ? 1 : 0); }
+void tile_set_gemm_tile_min(int min_tiles) { g_gemm_tile_min = min_tiles < 0 ? -1 : min_tiles; }
 void tile_set_trace(int64_t cap) { g_trace_cap = cap > 0 ? cap : 0; }
 void tile_set_ctas(int ctas) { g_ctas = ctas > 0 ? ctas : 0; }
 

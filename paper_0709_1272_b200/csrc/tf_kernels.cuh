@@ -698,6 +698,30 @@ __device__ inline void gemm_body(const Ctx& cx, const double* A, const double* B
   TF_PROBE_MARK(2, t0);
 }
 
+// GEMM, the whole tile C -= A B^T as one work item (b a multiple of 128, operands 16-byte
+// aligned): the nr x nr sub-tile products of gemm_body run as one continuous slice stream
+// (Gemm::chain2_mb), row strip by row strip.  Same arithmetic per sub-tile as gemm_body.
+// Used by the panel-level Cholesky graph for the updates of steps with enough tiles to keep
+// every SM busy with whole-tile items (tf_host.cpp).
+__device__ inline void gemm_tile_body(const Ctx& cx, const double* A, const double* B, double* C, double* sm) {
+  const int b = cx.b;
+  const int nr = b / RB;
+  GemmNT128 g;
+  g.chain2_mb<2>(sm, A, b, B, b, nr * nr, nr, b, [&](int x) {
+    // the C strip of the products about to start: into L2 ahead of their epilogues
+    if (x < 0 || (x + 1) % nr == 0) {
+      const int mi = (x + 1) / nr;
+      if (mi < nr)
+        for (int nj = 0; nj < nr; ++nj) prefetch_l2(C + mi * RB + (size_t)(nj * RB) * b, b, RB, RB);
+    }
+    if (x >= 0) {
+      const int mi = x / nr, nj = x - mi * nr;
+      sub_store(g, C + mi * RB + (size_t)(nj * RB) * b, b, RB, RB, false, 0, 0, /*red=*/true);
+    }
+    g.zero();
+  });
+}
+
 TF_DEF_REF_RET(v_potrf_left, potrf_left, (Ctx cx, double* A), (cx, A, dsm))
 TF_DEF_REF_RET(v_potrf_right, potrf_right, (Ctx cx, double* A), (cx, A, dsm))
 TF_DEF_REF(v_trsm_left, trsm_left, (Ctx cx, const double* L, double* X, int item), (cx, L, X, item, dsm))
@@ -707,6 +731,7 @@ TF_DEF_REF_RET(v_potrf_blocked, potrf_blocked, (Ctx cx, double* A), (cx, A, dsm)
 TF_DEF_REF(v_trsm_128, trsm_128, (Ctx cx, const double* L, double* X), (cx, L, X, dsm))
 TF_DEF_REF(v_syrk, syrk_body, (Ctx cx, const double* A, double* C, int item), (cx, A, C, item, dsm))
 TF_DEF_REF(v_gemm, gemm_body, (Ctx cx, const double* A, const double* B, double* C, int item), (cx, A, B, C, item, dsm))
+TF_DEF_REF(v_gemm_tile, gemm_tile_body, (Ctx cx, const double* A, const double* B, double* C), (cx, A, B, C, dsm))
 
 // Cholesky task kernels (the `sm` argument is the caller's dynamic shared memory; the
 // variants re-declare it).  POTRF / TRSM: right-looking over 128-column panels for b a

@@ -19,7 +19,8 @@ KINDS = {"potrf": 0, "trsm": 1, "syrk": 2, "gemm": 3, "geqrt": 4, "larfb": 5, "t
 SOLVE_KINDS = {"unitl": 14, "xgessm": 15, "xssssm": 16, "xlarfb": 17, "xssrfb": 18, "xtrsmu": 19, "xgemm": 20,
                "xunssssm": 21, "xungessm": 22}
 SLAB_KINDS = {"geqrt_s": 25, "tsqrt_s": 26, "getrf_s": 27, "tstrf_s": 28,  # slab-level DAG panel tasks
-              "tsqrt_a": 29, "tstrf_a": 30}  # ... and their off-chain apply tasks
+              "tsqrt_a": 29, "tstrf_a": 30,  # ... and their off-chain apply tasks
+              "potrf_d": 31, "potrf_b": 32, "trsm_p": 33}  # panel-level Cholesky DAG (128-column panels)
 KIND_NAMES = {v: k for k, v in KINDS.items()}
 KIND_NAMES.update({v: k for k, v in SLAB_KINDS.items()})
 ALGS = {"chol": 0, "qr": 1, "lu": 2, "getrs": 3, "ormqr": 4, "qrs": 5, "lu_apply_N": 6}
@@ -56,6 +57,7 @@ def _load():
         "tile_factor_host": (i32, [i32, i64, i64, i64, vp, vp, vp, vp, vp]),
         "tile_set_policy": (None, [i32]),
         "tile_set_slab_dag": (None, [i32]),
+        "tile_set_gemm_tile_min": (None, [i32]),
         "tile_set_trace": (None, [i64]),
         "tile_trace_fetch": (i64, [vp, i64]),
         "tile_set_ctas": (None, [i32]),
@@ -90,7 +92,8 @@ SYMBOLS = [
     "tile_chol", "tile_qr", "tile_lu", "tile_qr_mn", "tile_lu_mn", "tile_mn_aux_elems", "tile_mn_ipiv_elems",
     "tile_lu_nopiv", "tile_getrs", "tile_ormqr", "tile_qrs", "tile_lu_apply_N",
     "tile_qr_t_elems", "tile_lu_l_elems", "tile_lu_ipiv_elems",
-    "tile_pack", "tile_unpack", "tile_factor_host", "tile_set_policy", "tile_set_slab_dag", "tile_set_trace",
+    "tile_pack", "tile_unpack", "tile_factor_host", "tile_set_policy", "tile_set_slab_dag", "tile_set_gemm_tile_min",
+    "tile_set_trace",
     "tile_trace_fetch", "tile_set_ctas", "tile_dag_export", "tile_dag_export_slab", "tk_run", "tile_dist_open",
     "tile_dist_ipc_bytes", "tile_dist_connect", "tile_dist_factor", "tile_dist_close",
     "tile_dist_probe", "tile_dist_probe_read",
@@ -280,6 +283,12 @@ def tile_set_policy(policy: int) -> None:
 def tile_set_slab_dag(on: int) -> None:
     """1 = slab-level QR / LU task graph (default), 0 = tile-level, -1 = default."""
     lib.tile_set_slab_dag(int(on))
+
+
+def tile_set_gemm_tile_min(min_tiles: int) -> None:
+    """Panel-level Cholesky graph: whole-tile GEMM items while a step has >= min_tiles tiles
+    outside the lookahead column (0 = strip items everywhere, -1 = default)."""
+    lib.tile_set_gemm_tile_min(int(min_tiles))
 
 
 def tile_set_trace(cap: int) -> None:

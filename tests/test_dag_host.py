@@ -546,13 +546,26 @@ def _chol_panel_rw(kind, k, i, j, J, nr):
     return full(i, k) + full(j, k), full(i, j)
 
 
-@pytest.mark.parametrize("p,b", [(5, 256), (4, 384), (4, 512), (3, 1024)])
-def test_chol_panel_dag_orders_every_hazard(p, b):
+@pytest.mark.parametrize("p,b,tile_min", [(5, 256, -1), (4, 384, -1), (4, 512, -1), (3, 1024, -1),
+                                          (6, 512, 1), (7, 256, 3), (5, 512, 0)])
+def test_chol_panel_dag_orders_every_hazard(p, b, tile_min):
     """Soundness of the panel-level Cholesky graph: every RAW / WAR / WAW
     conflict of the independent 128 x 128 block model above is ordered by a path of the
-    exported graph, and the graph has the expected task census."""
-    d = tf.tile_dag_export_slab("chol", p, b, 32)
+    exported graph, and the graph has the expected task census; also with whole-tile GEMM
+    items (tile_set_gemm_tile_min: one item, slab column = 1) in the steps that have at
+    least tile_min GEMM tiles outside the lookahead column."""
+    tf.tile_set_gemm_tile_min(tile_min)
+    try:
+        d = tf.tile_dag_export_slab("chol", p, b, 32)
+    finally:
+        tf.tile_set_gemm_tile_min(-1)
     nr = b // 128
+    whole = [t for t in range(len(d["kind"])) if int(d["kind"][t]) == 3 and int(d["slab"][t]) == 1]
+    tm = 296 if tile_min < 0 else tile_min
+    want = sum((p - k - 2) * (p - k - 3) // 2 for k in range(p)
+               if tm > 0 and p - k - 1 >= 3 and (p - k - 2) * (p - k - 3) // 2 >= tm)
+    assert len(whole) == want
+    assert all(int(d["j"][t]) > int(d["k"][t]) + 1 for t in whole)
     nt = len(d["kind"])
     kinds = [int(x) for x in d["kind"]]
     assert kinds.count(31) == p * nr and kinds.count(32) == p * (nr - 1)

@@ -43,6 +43,25 @@ def test_slab_dag_bitwise_equals_tile_dag(alg, n, b, ib, seed):
     assert i0 == i1 == 0
 
 
+@pytest.mark.parametrize("n,b,tile_min", [(4096, 512, 1), (3072, 256, 10), (3072, 384, 3)])
+def test_panel_dag_whole_tile_gemm_bitwise(n, b, tile_min):
+    """Whole-tile GEMM items (one slice stream over the nr x nr sub-tile products) give the
+    same bits as the strip items and as the tile-level graph."""
+    A = tilegen.spd(n, 12)
+    outs = []
+    for fine, tm in ((0, -1), (1, 0), (1, tile_min)):
+        tf.tile_set_slab_dag(fine)
+        tf.tile_set_gemm_tile_min(tm)
+        try:
+            outs.append(gpu_factor("chol", A, b, 32))
+        finally:
+            tf.tile_set_slab_dag(-1)
+            tf.tile_set_gemm_tile_min(-1)
+    for G, _, _, info in outs[1:]:
+        assert info == 0
+        assert np.array_equal(G.view(np.int64), outs[0][0].view(np.int64))
+
+
 @pytest.mark.parametrize("col", [70, 300, 512 + 130, 1023])
 def test_panel_dag_chol_not_spd_info(col):
     """A non-positive pivot inside a later 128-column panel / tile: info comes from the

@@ -30,13 +30,15 @@ def test_trace_respects_dag(alg, n, b, ib, slab):
     A = {"chol": tilegen.spd, "qr": tilegen.uniform, "lu": tilegen.normal}[alg](n, 3)
     tf.tile_set_trace(1 << 22)
     tf.tile_set_slab_dag(slab)
+    tf.tile_set_gemm_tile_min(1 if slab else -1)  # panel-level Cholesky: whole-tile GEMM items too
     try:
         gpu_factor(alg, A, b, ib)
         rec = tf.tile_trace_fetch()
+        d = tf.tile_dag_export_slab(alg, n // b, b, ib) if slab else tf.tile_dag_export(alg, n // b)
     finally:
         tf.tile_set_trace(0)
         tf.tile_set_slab_dag(-1)
-    d = tf.tile_dag_export_slab(alg, n // b, b, ib) if slab else tf.tile_dag_export(alg, n // b)
+        tf.tile_set_gemm_tile_min(-1)
     nt = len(d["kind"])
     task, item, start, end = rec[:, 0], rec[:, 1], rec[:, 3], rec[:, 4]
     assert len(rec) > 0 and (end >= start).all()

@@ -14,5 +14,5 @@ done
 CMD="python bench.py --steps 1 --warmup 1 --only --no-e2e --no-cpu"
 timeout 600 $CMD > gpurun_out/plain_c4.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_c4.csv $CMD > gpurun_out/ncu_launch_c4.log 2>&1; echo "launches rc=$?"
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:tf_persistent -s 1 -c 1 -o gpurun_out/prof_c4_r02b $CMD > gpurun_out/ncu_full_c4.log 2>&1; echo "full rc=$?"
-ncu -i gpurun_out/prof_c4_r02b.ncu-rep --page raw --csv > gpurun_out/prof_c4_r02b_raw.csv 2>/dev/null
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:tf_persistent -s 1 -c 1 -o gpurun_out/prof_c4_${TAG:-r02b} $CMD > gpurun_out/ncu_full_c4.log 2>&1; echo "full rc=$?"
+ncu -i gpurun_out/prof_c4_${TAG:-r02b}.ncu-rep --page raw --csv > gpurun_out/prof_c4_${TAG:-r02b}_raw.csv 2>/dev/null

@@ -79,7 +79,8 @@ def main():
     bench.factor(tf, cfg, work, aux, piv, info)
     rec = tf.tile_trace_fetch()
     tf.tile_set_trace(0)
-    fine = cfg["kind"] != "chol" and os.environ.get("TF_FINE", "1") != "0" and b in (128, 256, 512) and ib in (32, 64)
+    fine = os.environ.get("TF_FINE", "1") != "0" and (
+        (b >= 256 and b % 128 == 0) if cfg["kind"] == "chol" else (b in (128, 256, 512) and ib in (32, 64)))
     d = tf.tile_dag_export_slab(cfg["kind"], n // b, b, ib, a.policy) if fine else tf.tile_dag_export(cfg["kind"], n // b, a.policy)
     kinds = d["kind"][rec[:, 0]]
     t0 = rec[:, 3].min()
@@ -107,6 +108,10 @@ def main():
         nit = int(rec[m, 1].max()) + 1  # items per task of this kind
         if name.endswith("_a"):  # off-chain apply of older inner blocks to one slab
             fl = 0.0
+        elif name in ("potrf_d", "potrf_b"):  # one 128 x 128 block of a panel (flops vary with the panel)
+            fl = 0.0
+        elif name == "trsm_p":  # mean over the panels of a 128-row block
+            fl = item_flops("trsm", b, ib, (b // 128) ** 2)
         elif name.endswith("_s"):  # slab-level panel task: one 32-column slab of the tile
             fl = item_flops(name[:-2], b, ib, b // 32)
         else:
@@ -114,6 +119,14 @@ def main():
         out["kinds"][name] = {"items": int(m.sum()), "mean_us": float(dur[m].mean()), "max_us": float(dur[m].max()),
                               "gflops_per_sm": float(fl / (dur[m].mean() * 1e-6) / 1e9),
                               "sm_time_share": float(dur[m].sum() / dur.sum())}
+    # SM occupancy over time: busy fraction in 20 equal windows of the makespan
+    edges = np.linspace(0.0, span, 21)
+    occ = []
+    for w in range(20):
+        lo, hi = edges[w], edges[w + 1]
+        occ.append(float(np.clip(np.minimum(end, hi) - np.maximum(start, lo), 0, None).sum() / (nsm * (hi - lo))))
+    out["busy_by_window"] = [round(x, 3) for x in occ]
+    out["idle_ms_by_window"] = [round((1 - x) * span / 20 / 1e3, 2) for x in occ]
     # the realised critical chain: from the last task to finish, repeatedly step to the
     # predecessor that finished last; time on the chain split into task work and waiting
     tids = rec[:, 0].astype(np.int64)

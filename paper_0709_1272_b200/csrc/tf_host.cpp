@@ -266,14 +266,17 @@ void global_tasks_fine(int alg, int p, int b, int ib, int policy, std::vector<Ta
 // before it.)  The per-step chain POTRF -> TRSM shrinks from the whole POTRF plus a whole
 // TRSM to 2 nr - 1 block kernels plus one TRSM panel; every element sees the same
 // operations in the same order as in the tile-level DAG (results are bitwise identical).
-// GEMM(k,i,j) outside the lookahead column runs as ONE whole-tile item (pad = 1,
-// gemm_tile_body: the nr x nr sub-tile products as one slice stream) while step k has at
-// least TF_GEMM_TILE_MIN (default 296 = 2 x 148 SMs) such tiles, so the per-item costs
-// (scheduler round trip, pipeline fill, last epilogue) are paid once per tile; later steps
-// and the lookahead column keep the finer strip items for load balance and latency.
-int g_gemm_tile_min = -1;  // tile_set_gemm_tile_min: -1 = default (TF_GEMM_TILE_MIN env, else 296)
+// Optional (tile_set_gemm_tile_min / TF_GEMM_TILE_MIN = t > 0; default off): GEMM(k,i,j)
+// outside the lookahead column runs as ONE whole-tile item (pad = 1, gemm_tile_body: the
+// nr x nr sub-tile products as one slice stream) while step k has at least t such tiles, so
+// the per-item costs (scheduler round trip, pipeline fill, last epilogue) are paid once per
+// tile; later steps and the lookahead column keep the finer strip items.  Measured on
+// config 4 with t = 296: 386.4 -> 385.4 ms but DRAM traffic 344 -> 430 GB per launch (the four
+// strip items of a tile run on neighbouring CTAs at the same time and share B through L2;
+// whole-tile items each stream their own 6 MB): not worth it, so it is off by default.
+int g_gemm_tile_min = -1;  // tile_set_gemm_tile_min: -1 = default (TF_GEMM_TILE_MIN env, else 0 = off)
 int gemm_tile_min() {
-  static const int env = getenv("TF_GEMM_TILE_MIN") ? atoi(getenv("TF_GEMM_TILE_MIN")) : 296;
+  static const int env = getenv("TF_GEMM_TILE_MIN") ? atoi(getenv("TF_GEMM_TILE_MIN")) : 0;
   return g_gemm_tile_min >= 0 ? g_gemm_tile_min : env;
 }
 

@@ -561,7 +561,7 @@ def test_chol_panel_dag_orders_every_hazard(p, b, tile_min):
         tf.tile_set_gemm_tile_min(-1)
     nr = b // 128
     whole = [t for t in range(len(d["kind"])) if int(d["kind"][t]) == 3 and int(d["slab"][t]) == 1]
-    tm = 296 if tile_min < 0 else tile_min
+    tm = 0 if tile_min < 0 else tile_min  # default: off
     want = sum((p - k - 2) * (p - k - 3) // 2 for k in range(p)
                if tm > 0 and p - k - 1 >= 3 and (p - k - 2) * (p - k - 3) // 2 >= tm)
     assert len(whole) == want

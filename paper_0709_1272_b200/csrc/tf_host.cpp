@@ -287,8 +287,9 @@ void global_tasks_chol_panel(int p, int b, int policy, std::vector<TaskD>& tasks
   std::unordered_map<uint64_t, int> id;
   id.reserve((size_t)p * p * p / 2 + 16);
   tasks.clear();
-  // local kind codes for the key: 0 PD, 1 PB, 2 TP, 3 SYRK, 4 GEMM; panel in the low 3 bits of j
-  auto key = [&](int lk, int k, int i, int j, int J) { return key4(lk, k, i, j * 8 + J); };
+  // local kind codes for the key: 0 PD, 1 PB, 2 TP, 3 SYRK, 4 GEMM; panel in the low 6 bits of
+  // j (nr <= 32 for b <= TF_MAX_B = 4096)
+  auto key = [&](int lk, int k, int i, int j, int J) { return key4(lk, k, i, j * 64 + J); };
   auto add = [&](int lk, int kind, int k, int i, int j, int J, int nit, int pad = -1) {
     TaskD d{kind, k, i, j, nit, 0, level_of(coarse_kind(kind), k, j, policy), pad >= 0 ? pad : J};
     id[key(lk, k, i, j, J)] = (int)tasks.size();

@@ -547,7 +547,7 @@ def _chol_panel_rw(kind, k, i, j, J, nr):
 
 
 @pytest.mark.parametrize("p,b,tile_min", [(5, 256, -1), (4, 384, -1), (4, 512, -1), (3, 1024, -1),
-                                          (6, 512, 1), (7, 256, 3), (5, 512, 0)])
+                                          (6, 512, 1), (7, 256, 3), (5, 512, 0), (3, 1280, -1), (3, 1152, 1)])
 def test_chol_panel_dag_orders_every_hazard(p, b, tile_min):
     """Soundness of the panel-level Cholesky graph: every RAW / WAR / WAW
     conflict of the independent 128 x 128 block model above is ordered by a path of the

@@ -31,7 +31,8 @@ def _both(fn):
                                              ("lu", 2048, 256, 64, 6),
                                              # panel-level Cholesky graph (b a multiple of 128, >= 256)
                                              ("chol", 2048, 512, 64, 7), ("chol", 1280, 256, 32, 8),
-                                             ("chol", 1152, 384, 32, 9), ("chol", 2048, 1024, 64, 10)])
+                                             ("chol", 1152, 384, 32, 9), ("chol", 2048, 1024, 64, 10),
+                                             ("chol", 1920, 640, 32, 13), ("chol", 2304, 1152, 32, 14)])
 def test_slab_dag_bitwise_equals_tile_dag(alg, n, b, ib, seed):
     A = {"chol": tilegen.spd, "qr": tilegen.uniform, "lu": tilegen.normal}[alg](n, seed)
     (G0, X0, P0, i0), (G1, X1, P1, i1) = _both(lambda: gpu_factor(alg, A, b, ib))

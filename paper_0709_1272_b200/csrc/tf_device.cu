@@ -133,12 +133,23 @@ __device__ inline int sched_pop(const Sched& S, const Dist& D, int* info) {
       const int h = hv[lev];
       const int t = tv[lev];
       if (h < t) {
-        if (atomicCAS(&S.head[lev], h, h + 1) == h) {
-          const volatile int* slot = S.q + S.qbase[lev] + h;
+        // With a backlog of at least two items per CTA nobody can over-claim, so the head is
+        // taken by an unconditional fetch-add: no CAS retry round trips when many CTAs finish
+        // equal items at the same moment (every CTA holds at most one claim at a time).
+        int hh = h;
+        bool got;
+        if (t - h >= 2 * (int)gridDim.x) {
+          hh = atomicAdd(&S.head[lev], 1);
+          got = true;
+        } else {
+          got = atomicCAS(&S.head[lev], h, h + 1) == h;
+        }
+        if (got) {
+          const volatile int* slot = S.q + S.qbase[lev] + hh;
           int v;
           while ((v = *slot) < 0) {
           }
-          TF_ASSERT(v < S.nitems, "popped item %d >= nitems %d (level %d slot %d)", v, S.nitems, lev, h);
+          TF_ASSERT(v < S.nitems, "popped item %d >= nitems %d (level %d slot %d)", v, S.nitems, lev, hh);
           // acquire: the producers' tile writes are visible (and L1 is invalidated); peer
           // GPUs' stores into the receive cache need the system-scope fence
           if (D.nranks > 1) fence_ar_sys();

@@ -63,6 +63,26 @@ def test_panel_dag_whole_tile_gemm_bitwise(n, b, tile_min):
         assert np.array_equal(G.view(np.int64), outs[0][0].view(np.int64))
 
 
+def test_panel_dag_schedule_independent():
+    """The panel-level Cholesky graph gives the same bits for any grid size, priority policy
+    and run (several CTAs now work inside one POTRF / TRSM; every block still sees its
+    operations in one fixed order), and a one-CTA grid completes (no CTA ever waits for a
+    specific task)."""
+    n, b = 2048, 512
+    A = tilegen.spd(n, 15)
+    ref = gpu_factor("chol", A, b, 64)[0].view(np.int64)
+    try:
+        for ctas, policy in ((1, 1), (3, 0), (7, 1), (40, 0), (148, 0), (0, 1)):
+            tf.tile_set_ctas(ctas)
+            tf.tile_set_policy(policy)
+            for _ in range(2):
+                G, _, _, info = gpu_factor("chol", A, b, 64)
+                assert info == 0 and np.array_equal(G.view(np.int64), ref), (ctas, policy)
+    finally:
+        tf.tile_set_ctas(0)
+        tf.tile_set_policy(1)
+
+
 @pytest.mark.parametrize("col", [70, 300, 512 + 130, 1023])
 def test_panel_dag_chol_not_spd_info(col):
     """A non-positive pivot inside a later 128-column panel / tile: info comes from the
